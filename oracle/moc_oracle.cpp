@@ -41,21 +41,26 @@ struct Err {
 };
 
 // ---------------------------------------------------------------------------
-// epsilon-merge of a sorted boundary list (App. A.7; reading Q22):
-// every raw segment shorter than eps joins the preceding merged segment; a
-// leading short segment joins the first long one.  Returns merged intervals.
+// epsilon-merge of a sorted boundary list (App. A.7; readings Q22, Q22b):
+// every raw segment shorter than eps joins the preceding merged segment; the
+// leading run of short raw segments joins the first long one (so the merged
+// list read backwards is the merge of the reversed raw list).  Returns merged
+// intervals.
 // ---------------------------------------------------------------------------
 void merge_segments(const std::vector<double>& b, std::vector<std::pair<double, double>>& out) {
   out.clear();
+  bool lead = true;  // everything merged so far is a run of short raw segments
   for (size_t q = 0; q + 1 < b.size(); ++q) {
     double a0 = b[q], a1 = b[q + 1];
     double len = a1 - a0;
     if (out.empty()) {
       out.push_back({a0, a1});
+      lead = len < kEpsL;
     } else if (len < kEpsL) {
       out.back().second = a1;
-    } else if (out.size() == 1 && (out[0].second - out[0].first) < kEpsL) {
-      out[0].second = a1;  // first (short) segment merges forward
+    } else if (lead) {
+      out.back().second = a1;  // leading short run merges forward
+      lead = false;
     } else {
       out.push_back({a0, a1});
     }
