@@ -1,0 +1,224 @@
+/*
+ * moc3d.h — C ABI of libmoc3d.so, the B200-native OTF 3D MOC transport sweep
+ * (arXiv 2503.17743) and the power iteration that wraps it.
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n (reference text),
+ * SURVEY §x = /root/repo/SURVEY.md, Qn = reading n in DESIGN.md §2.
+ *
+ * Conventions (all entry points):
+ *   - Return value: MOC_OK (0) on success, a negative MOC_E_* code on error; the
+ *     message is available from moc_last_error()/moc_solver_last_error() until
+ *     the next call on the same handle.  No C++ exception crosses the ABI.
+ *   - Units: cm and 1/cm.  Host arrays are fp64 unless stated; every input array
+ *     is COPIED on entry — the caller keeps ownership and may free it on return.
+ *   - Output arrays are caller-allocated host buffers whose sizes come from the
+ *     query calls (moc_num_fsrs, moc_get_track_stats).
+ *   - Handles own all host and device memory they allocate.  A handle is not
+ *     thread-safe; distinct handles are independent.
+ *   - Device work is stream-ordered on the stream given to moc_solver_create
+ *     (pass torch.cuda.current_stream().cuda_stream, or NULL for the legacy stream).
+ *   - Faces: 0 x-, 1 x+, 2 y-, 3 y+, 4 z-, 5 z+ ; bc 0 = vacuum, 1 = reflective.
+ *   - 3D track id: Alg. 1 order: 2D track t outer, polar n, stack member i.
+ *     Slot = 2*track + dir, dir 0 = forward (increasing 2D s), 1 = backward.
+ */
+#ifndef MOC3D_H
+#define MOC3D_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MOC_OK = 0,
+  MOC_E_INVALID_ARG = -1, /* NULL / out-of-range argument                                  */
+  MOC_E_GEOMETRY = -2,    /* radii overlap the cell, point out of domain       */
+  MOC_E_REFERENCE = -3,   /* unknown material index                                  */
+  MOC_E_MESH = -4,        /* axial planes not strictly increasing / planes[0] != 0   */
+  MOC_E_PARAM = -5,       /* num_azim % 4, spacing > domain, G > 8, odd num_polar    */
+  MOC_E_TRACE = -6,       /* segmentation stall, 3D link landing off a stack member */
+  MOC_E_CAPACITY = -7,    /* device memory exhausted                                */
+  MOC_E_EIGEN = -8,       /* k <= 0 or zero fission source                    */
+  MOC_E_NUMERIC = -9,     /* NaN / negative scalar flux                              */
+  MOC_E_NOCONV = -10,     /* max_iter reached without convergence                    */
+  MOC_E_CUDA = -11,       /* CUDA runtime error                                              */
+  MOC_E_NCCL = -12,       /* collective error                                                */
+  MOC_E_STATE = -13       /* call order (e.g. tracks not generated)                          */
+};
+
+typedef struct moc_problem moc_problem;
+typedef struct moc_solver moc_solver;
+
+/* ---------------------------------------------------------------- problem
+ * Geometry/material setup ("geometric modelling").       */
+int moc_problem_create(moc_problem** out);
+void moc_problem_destroy(moc_problem* p);
+const char* moc_last_error(const moc_problem* p);
+
+/* Multigroup materials.  sigma_t [n_mat][G], sigma_s [n_mat][G from][G to],
+ * nu_sigma_f [n_mat][G], chi [n_mat][G].  Requires sigma_t > 0, G in [1, 8];
+ * chi must sum to 1 +- 1e-9 for fissile materials (MOC_E_PARAM otherwise). */
+int moc_set_materials(moc_problem* p, int32_t n_mat, int32_t G, const double* sigma_t,
+                      const double* sigma_s, const double* nu_sigma_f, const double* chi);
+
+/* Axially extruded pin lattice ("axially extruded geometry").
+ * Cells are nx*ny rectangles of pitch (pitch_x, pitch_y), row-major from (x_min, y_min).
+ * Cell type c has n_rings[c] concentric circles (radii[c*max_rings + q], ascending,
+ * < min(pitch)/2) centred in the cell; local region q < n_rings is the q-th ring
+ * (innermost first), local region n_rings[c] is the moderator outside the last circle.
+ * material[(c*(max_rings+1) + q)*n_zones + zone] is the material of local region q
+ * in axial zone `zone`; zone_of_layer[l] maps axial layer l (between planes[l] and
+ * planes[l+1]; planes[0] must be 0) to its zone.
+ * FSR numbering: region r = prefix(cell) + local, j = r*n_layers + layer. */
+typedef struct {
+  int32_t nx, ny;
+  double pitch_x, pitch_y;
+  const int32_t* cell_type;     /* [ny*nx]            */
+  int32_t n_types, max_rings;
+  const int32_t* n_rings;       /* [n_types]          */
+  const double* radii;          /* [n_types*max_rings] (may be NULL if max_rings == 0) */
+  int32_t n_layers;
+  const double* planes;         /* [n_layers+1]       */
+  int32_t n_zones;
+  const int32_t* zone_of_layer; /* [n_layers]         */
+  const int32_t* material;      /* [n_types*(max_rings+1)*n_zones] */
+  int32_t bc[6];
+} moc_geometry_desc;
+int moc_set_geometry(moc_problem* p, const moc_geometry_desc* g);
+int moc_num_fsrs(const moc_problem* p, int64_t* J);
+/* FSR containing (x, y, z) (axial slabs half-open, top slab closed). */
+int moc_fsr_of_point(const moc_problem* p, double x, double y, double z, int64_t* fsr);
+
+/* 2D cyclic laydown + 2D segmentation (A1) and z-stacks + 3D links (A2), on the host
+ * ("the CPU executes 2D ray tracing").  num_azim % 4 == 0,
+ * num_polar even, spacings > 0. */
+typedef struct {
+  int32_t num_azim, num_polar;
+  double radial_spacing, axial_spacing;
+} moc_track_params;
+int moc_generate_tracks(moc_problem* p, const moc_track_params* tp);
+
+typedef struct {
+  int64_t n_fsr, n_regions, n_tracks2d, n_segs2d, n_stacks, n_tracks3d, n_cycles;
+  int64_t n_segs3d_raw; /* upper bound: #2D segments spanned + #axial planes crossed */
+} moc_track_stats;
+int moc_get_track_stats(const moc_problem* p, moc_track_stats* st);
+
+/* Debug/parity exports of the laydown (caller-allocated, sizes from moc_get_track_stats).
+ * tracks2d: azim[T2], xy0[2*T2], xy1[2*T2], length[T2], seg_off[T2+1],
+ *           link_fwd/link_bwd[T2] (target 2D track or -1 vacuum), *_enters_fwd[T2]. */
+int moc_get_tracks2d(const moc_problem* p, int32_t* azim, double* xy0, double* xy1, double* length,
+                     int64_t* seg_off, int64_t* link_fwd, int32_t* link_fwd_enters_fwd,
+                     int64_t* link_bwd, int32_t* link_bwd_enters_fwd);
+int moc_get_segments2d(const moc_problem* p, int64_t* region, double* s_end);
+/* per stack (t, n) in Alg. 1 order: z of member 0 at s = 0, member count, first 3D id [S+1] */
+int moc_get_stacks(const moc_problem* p, double* z0, int64_t* count, int64_t* first);
+/* per (a, n): corrected polar angle, axial spacing dz, weight W, perpendicular area A_perp */
+int moc_get_polar(const moc_problem* p, double* theta, double* dz, double* weight, double* aperp);
+/* 3D link table by index arithmetic: link[slot] = target slot or -1. */
+int moc_get_links3d(const moc_problem* p, int64_t* link);
+
+/* OTF 3D segments of one track (S:231 trace_segments_otf; Eqs. 5, 8, 11) computed on
+ * the host with the same walk the device kernel runs.  Returns #segments in *nseg;
+ * if cap < *nseg nothing is written and MOC_E_INVALID_ARG is returned. */
+int moc_trace_track_3d(const moc_problem* p, int64_t track3d, int64_t* fsr, double* len,
+                       int64_t cap, int64_t* nseg);
+
+/* Eqs. 5-7 and 9-10 as stated, for tests and cost estimates.
+ * intersecting_range: i_start = ceil((zmin - max(z0s, z0e))/dz), i_end = floor((zmax - min(z0s, z0e))/dz);
+ * full_crossing_range: i_in = ceil((zmin - min)/dz), i_out = floor((zmax - max)/dz). */
+double moc_z_of(double z0, double dz, int64_t i, double theta, double s);
+void moc_intersecting_range(double z0_sstart, double z0_send, double dz, double zmin, double zmax,
+                            int64_t* i_start, int64_t* i_end);
+void moc_full_crossing_range(double z0_sstart, double z0_send, double dz, double zmin, double zmax,
+                             int64_t* i_in, int64_t* i_out);
+/* Eq. 13 flattened Z-STACK accessor: stack[z[i] + j*c + k]. */
+int64_t moc_flat_index(const int64_t* offsets, int64_t c, int64_t i, int64_t j, int64_t k);
+
+/* Paper §4.2 / §4.3 host scheduling rules.
+ * serpentine: sort by count descending (stable), reverse every odd chunk. */
+int moc_serpentine_order(const int64_t* counts, int64_t n, int64_t chunk, int64_t* order_out);
+/* EXP/OTF partition: descending by estimate, accumulate while <= fraction*budget. */
+int moc_partition_exp_otf(const int64_t* estimates, int64_t n, double budget, double fraction,
+                          int32_t* preload_out);
+
+/* ---------------------------------------------------------------- solver */
+typedef struct {
+  int32_t rank, world;      /* world == 1: single GPU                                 */
+  int32_t exchange_on_host; /* reserved (0)                                           */
+} moc_comm_desc;
+
+typedef struct {
+  int32_t schedule;     /* 0 = persistent cost-sorted stack-band units (default),
+                           1 = Alg. 2 grid-stride over 3D tracks in Alg. 1 order (paper baseline),
+                           2 = Alg. 2 over tracks sorted by segment count with the §4.3 serpentine */
+  int32_t threads, blocks;  /* Alg. 2 launch shape (P:146 default 512 x 512); 0 = default */
+  int32_t deterministic;    /* reserved (0) */
+} moc_solver_opts;
+
+/* Upload the laydown to `device`, allocate HBM state (boundary psi double buffer,
+ * FSR arrays), compute track-based FSR volumes and exact per-track segment counts on
+ * the device.  comm == NULL means one GPU; with world > 1 this rank sweeps its
+ * contiguous cost-balanced share of the stacks. */
+int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_stream,
+                      const moc_comm_desc* comm, const moc_solver_opts* opts);
+int moc_solver_destroy(moc_solver* s);
+const char* moc_solver_last_error(const moc_solver* s);
+
+/* Run n_iter power iterations (A3..A7 on the device; A8 is driven by the caller through
+ * moc_solver_comm_buffers when world > 1).  Initial state phi = 1, k = 1, psi = 0 (Q11).
+ * Writes the final k and fission-source residual. Stream-ordered; synchronises the
+ * stream once at the end to read k (16 bytes D2H). */
+int moc_iterate(moc_solver* s, int32_t n_iter, double* k_out, double* residual_out);
+
+typedef struct { double tol_k, tol_src; int32_t max_iter, check_every; } moc_solve_opts;
+typedef struct { double k; double residual; int32_t iterations; int32_t converged; } moc_result;
+/* Iterate until |dk| < tol_k and residual < tol_src.  MOC_E_NOCONV if max_iter hit. */
+int moc_solve(moc_solver* s, const moc_solve_opts* o, moc_result* r);
+int moc_reset(moc_solver* s); /* back to phi = 1, k = 1, psi = 0 */
+
+/* Replace the cross sections of a live solver (same n_mat, G; host fp64 arrays laid out
+ * as in moc_set_materials), e.g. for multiphysics feedback between outer iterations.
+ * Stream-ordered host->device copy (the flux state is kept). */
+int moc_solver_update_materials(moc_solver* s, const double* sigma_t, const double* sigma_s,
+                                const double* nu_sigma_f, const double* chi);
+
+/* Results (host, caller-owned). phi [J][G] normalised to sum_j V_j F_j = 1. */
+int moc_get_scalar_flux(moc_solver* s, double* phi);
+int moc_get_fsr_volumes(moc_solver* s, double* vol);
+int moc_get_history(moc_solver* s, double* k_hist, double* res_hist, int32_t cap, int32_t* n);
+int moc_get_balance(moc_solver* s, double* production, double* absorption, double* leakage);
+
+/* Device OTF walk per 3D track: merged segment count and FNV-1a-64 hash of the FSR id
+ * sequence (uint32 little-endian bytes), plus the sum of lengths (parity vs oracle). */
+int moc_device_trace_checksums(moc_solver* s, int64_t first, int64_t n, int32_t* nseg,
+                               uint64_t* hash, double* suml);
+
+typedef struct {
+  int64_t n_segs3d;          /* exact merged 3D segment count (device walk) */
+  int64_t n_integrations;    /* per sweep: 2 * n_segs3d * G */
+  double sweep_ms_last;      /* CUDA-event time of the last sweep kernel */
+  double iter_ms_last;       /* CUDA-event time of the last full iteration */
+  int64_t launches_per_iter; /* kernels launched per iteration */
+  double setup_ms;           /* moc_solver_create wall time */
+  int64_t device_bytes;      /* HBM allocated by this handle */
+} moc_timings;
+int moc_get_timings(moc_solver* s, moc_timings* t);
+
+/* Multi-GPU plumbing: device pointers of this rank's tally (fp32 [J][Gp],
+ * to be sum-all-reduced by the caller after each sweep) and of the halo send/recv
+ * buffers for cut-crossing boundary psi. */
+typedef struct {
+  void* tally; int64_t tally_elems;
+  void* halo_send; void* halo_recv; int64_t halo_elems;
+} moc_comm_buffers;
+int moc_solver_comm_buffers(moc_solver* s, moc_comm_buffers* b);
+
+/* Fine-grained iteration steps for the multi-GPU driver: sweep (A3-A6) then, after the
+ * caller's allreduce of the tally / halo exchange, finish (A7). */
+int moc_iteration_sweep(moc_solver* s);
+int moc_iteration_finish(moc_solver* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,48 @@
+"""Build libmoc3d.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+Host C++ (laydown, ABI) is compiled with -ffp-contract=off and no fast-math
+(App. A.7: host geometry must round the same way run to run); device code with
+-lineinfo so ncu's source page maps to csrc/.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+SO = os.path.join(HERE, "libmoc3d.so")
+SOURCES = ["laydown.cpp", "capi.cpp", "solver.cu"]
+HEADERS = ["host.h", "otf.h"]
+ARCH = "-gencode=arch=compute_100a,code=sm_100a"
+
+
+def _stale() -> bool:
+    if not os.path.exists(SO):
+        return True
+    t = os.path.getmtime(SO)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [
+        os.path.join(HERE, "..", "include", "moc3d.h"), __file__]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return SO
+    nvcc = os.environ.get("NVCC", "nvcc")
+    tmp = SO + ".tmp"
+    cmd = [nvcc, ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-o", tmp,
+           "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off,-fno-fast-math",
+           "-Xptxas", "-v" if verbose else "-O3",
+           "-lgomp"] + [os.path.join(CSRC, f) for f in SOURCES]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd, cwd=HERE)
+    os.replace(tmp, SO)
+    return SO
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(SO)

@@ -1,0 +1,968 @@
+// solver.cu — device side of libmoc3d.so: HBM layout, the OTF sweep kernels and
+// the per-iteration FSR kernels, plus the solver ABI.
+//
+// HBM layout (SoA):
+//   2D segments   seg_send f64[N2], seg_region u32[N2]       (A1, preloaded once)
+//   2D tracks     t_len f64, t_seg i64[T2+1], t_a i32
+//   (a, n)        cot, tan, 1/sin, dz f64; c = W A_perp f32
+//   z-stacks      st_z0 f64[S], st_first u32[S+1]            (Alg. 1 order)
+//   3D links      link u32[2*T3] (slot -> slot, ~0 = vacuum) (A6)
+//   work list     work u32[T3]                               (schedule, §4.3)
+//   boundary psi  psi f32[2][2*T3][GP]  (Jacobi double buffer, lazily normalised)
+//   FSR arrays    mat u8[J], qt f32[J][GP], phi f32[J][GP], tally f64[J][GP], vol f64[J]
+#include <cuda_runtime.h>
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/sequence.h>
+#include <thrust/sort.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "host.h"
+#include "otf.h"
+
+using namespace moc;
+
+#define CUDA_OK(x)                                                                              \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      throw Error(e_ == cudaErrorMemoryAllocation ? MOC_E_CAPACITY : MOC_E_CUDA,               \
+                  std::string(#x) + ": " + cudaGetErrorString(e_));                            \
+  } while (0)
+
+namespace {
+
+constexpr int kMaxMat = 32;
+constexpr int kMaxG = 8;
+constexpr double kFourPi = 12.566370614359172;
+
+__constant__ float c_sigt2[kMaxMat * kMaxG];     // sigma_t * log2(e)   (for ex2)
+__constant__ float c_sigt[kMaxMat * kMaxG];      // sigma_t
+__constant__ float c_nusf[kMaxMat * kMaxG];
+__constant__ float c_chi[kMaxMat * kMaxG];
+__constant__ float c_sigs[kMaxMat * kMaxG * kMaxG];  // [m][from][to]
+
+// device scalars (fp64): index map
+enum {
+  SC_K = 0,        // current k
+  SC_KPREV,        // k before the last update
+  SC_PROD_OLD,     // sum V F(phi) at the start of the iteration
+  SC_PROD_NEW,     // sum V F(phi_new) before normalisation
+  SC_SCALE,        // 1 / SC_PROD_NEW
+  SC_PSI_SCALE,    // scale applied to psi_in on read (lazy normalisation, Q12)
+  SC_RESID,        // RMS fission-source residual
+  SC_LEAK,         // vacuum outflow tally (unscaled) of the last sweep
+  SC_LEAK_SCALED,
+  SC_BAD,          // count of NaN/negative fluxes in the last finalize
+  SC_ITER,         // completed iterations
+  SC_N
+};
+
+struct DevData {
+  const double* seg_send;
+  const uint32_t* seg_region;
+  const double* planes;
+  int32_t NL;
+  double Z;
+  const double* t_len;
+  const int64_t* t_seg;
+  const int32_t* t_a;
+  const double *an_cot, *an_tan, *an_invsin, *an_dz;
+  const float* an_c;
+  const double* an_vw;  // W/(2 pi) * A_perp (volume weight)
+  const double* st_z0;
+  const uint32_t* st_first;
+  int32_t S, N;
+  uint32_t T3;
+};
+
+__device__ __forceinline__ int find_stack(const DevData& d, uint32_t id) {
+  int lo = 0, hi = d.S - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (d.st_first[mid] <= id) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ TrackGeo dev_track(const DevData& d, uint32_t id, int& stack, int& an) {
+  int s = find_stack(d, id);
+  int t = s / d.N, n = s - t * d.N;
+  an = d.t_a[t] * d.N + n;
+  stack = s;
+  TrackGeo g;
+  g.z0 = d.st_z0[s] + (double)(id - d.st_first[s]) * d.an_dz[an];
+  g.cot = d.an_cot[an];
+  g.tan = d.an_tan[an];
+  g.invsin = d.an_invsin[an];
+  g.L = d.t_len[t];
+  g.Z = d.Z;
+  g.sb = d.t_seg[t];
+  g.se = d.t_seg[t + 1];
+  return g;
+}
+
+__device__ __forceinline__ OtfView dev_view(const DevData& d) {
+  return OtfView{d.seg_send, d.seg_region, d.planes, d.NL};
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// ------------------------------------------------------------ setup kernels
+__global__ void k_volumes_costs(DevData d, double* vol, uint32_t* cost, unsigned long long* nseg_total) {
+  unsigned long long local = 0;
+  const OtfView v = dev_view(d);
+  for (uint32_t id = blockIdx.x * blockDim.x + threadIdx.x; id < d.T3; id += gridDim.x * blockDim.x) {
+    int s, an;
+    TrackGeo g = dev_track(d, id, s, an);
+    const double w = d.an_vw[an];
+    int n = otf_walk_fwd(v, g, [&](int64_t j, double len) { atomicAdd(&vol[j], w * len); });
+    cost[id] = (uint32_t)n;
+    local += (unsigned long long)n;
+  }
+  atomicAdd(nseg_total, local);
+}
+
+__global__ void k_checksums(DevData d, uint32_t first, uint32_t n, int32_t* nseg, unsigned long long* hash,
+                            double* suml) {
+  const OtfView v = dev_view(d);
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    int s, an;
+    TrackGeo g = dev_track(d, first + q, s, an);
+    uint64_t h = kFnvInit;
+    double sl = 0;
+    int c = otf_walk_fwd(v, g, [&](int64_t j, double len) {
+      h = fnv1a_step(h, (uint32_t)j);
+      sl += len;
+    });
+    nseg[q] = c;
+    hash[q] = h;
+    suml[q] = sl;
+  }
+}
+
+__global__ void k_serpentine(uint32_t* work, uint64_t n, uint64_t chunk) {
+  // reverse every odd chunk in place: thread per pair in odd chunks
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n; x += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t c = x / chunk;
+    if (!(c & 1)) continue;
+    uint64_t c0 = c * chunk, c1 = min(n, c0 + chunk);
+    uint64_t off = x - c0, len = c1 - c0;
+    if (off < len / 2) {
+      uint32_t a = work[c0 + off], b = work[c1 - 1 - off];
+      work[c0 + off] = b;
+      work[c1 - 1 - off] = a;
+    }
+  }
+}
+
+// ------------------------------------------------------------ A3: source
+// qtilde_j,g = [chi_g F_j / k + sum_g' Ss[g'->g] phi_j,g'] / (4 pi Sigma_t)   (Q2)
+// F_j = sum_g nuSf phi (for k and the residual); block partials of sum V F.
+template <int G, int GP>
+__global__ void k_source(int64_t J, const uint8_t* mat, const float* phi, const double* vol, const double* sc,
+                         float* qt, float* fold, double* part) {
+  __shared__ double red[32];
+  double acc = 0;
+  const double k = sc[SC_K];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
+    int m = mat[j];
+    float ph[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) ph[g] = phi[j * GP + g];
+    float F = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) F = fmaf(c_nusf[m * kMaxG + g], ph[g], F);
+    float fk = (float)(F / k);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float s = c_chi[m * kMaxG + g] * fk;
+#pragma unroll
+      for (int h = 0; h < G; ++h) s = fmaf(c_sigs[(m * kMaxG + h) * kMaxG + g], ph[h], s);
+      qt[j * GP + g] = s / ((float)kFourPi * c_sigt[m * kMaxG + g]);
+    }
+    fold[j] = F;
+    acc += vol[j] * (double)F;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+  }
+}
+
+// ------------------------------------------------------------ A4-A6: sweep (v1)
+// Alg. 2: grid-stride over 3D tracks in `work` order.  Each thread
+// walks its track forward then backward (Q24), applies Eq. 3 per segment and
+// group, accumulates c * dpsi into the FSR tally with fp64 atomics (Eq. 4, Q1),
+// and writes the outgoing psi into the linked slot of the other buffer (Q9).
+template <int G, int GP>
+__global__ void __launch_bounds__(256) k_sweep_v1(DevData d, const uint32_t* work, uint32_t nwork,
+                                                  const uint32_t* link, const uint8_t* mat, const float* qt,
+                                                  const float* psi_in, float* psi_out, double* tally, double* sc) {
+  const OtfView v = dev_view(d);
+  const float ps = (float)sc[SC_PSI_SCALE];
+  double leak = 0;
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwork; w += gridDim.x * blockDim.x) {
+    const uint32_t id = work[w];
+    int s, an;
+    TrackGeo g = dev_track(d, id, s, an);
+    const float c = d.an_c[an];
+    for (int dir = 0; dir < 2; ++dir) {
+      const uint32_t slot = 2 * id + dir;
+      float psi[G];
+#pragma unroll
+      for (int q = 0; q < G; ++q) psi[q] = psi_in[(size_t)slot * GP + q] * ps;
+      auto seg = [&](int64_t j, double len) {
+        const float Lf = (float)len;
+        const int m = mat[j];
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+          const float E = ex2_approx(-c_sigt2[m * kMaxG + q] * Lf);
+          const float dd = psi[q] - qt[j * GP + q];
+          const float dl = fmaf(-dd, E, dd);  // (psi - qtilde)(1 - e^{-tau})
+          psi[q] -= dl;
+          atomicAdd(&tally[j * GP + q], (double)(c * dl));
+        }
+      };
+      if (dir == 0) otf_walk_fwd(v, g, seg); else otf_walk_bwd(v, g, seg);
+      const uint32_t out = link[slot];
+      if (out != 0xffffffffu) {
+#pragma unroll
+        for (int q = 0; q < G; ++q) psi_out[(size_t)out * GP + q] = psi[q];
+      } else {
+        float e = 0;
+#pragma unroll
+        for (int q = 0; q < G; ++q) e += psi[q];
+        leak += (double)(c * e);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) leak += __shfl_xor_sync(0xffffffffu, leak, o);
+  if ((threadIdx.x & 31) == 0 && leak != 0.0) atomicAdd(&sc[SC_LEAK], leak);
+}
+
+// ------------------------------------------------------------ A7: finalize
+// phi_new = 4 pi qtilde + T / (Sigma_t V)   (Q2); block partials of sum V F(phi_new)
+template <int G, int GP>
+__global__ void k_finalize(int64_t J, const uint8_t* mat, const float* qt, const double* tally, const double* vol,
+                           float* phi, float* fnew, double* part, double* sc) {
+  __shared__ double red[32];
+  double acc = 0;
+  int bad = 0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
+    int m = mat[j];
+    double V = vol[j];
+    float F = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      double p = kFourPi * (double)qt[j * GP + g] + tally[j * GP + g] / ((double)c_sigt[m * kMaxG + g] * V);
+      float pf = (float)p;
+      if (!(pf >= 0.f)) ++bad;
+      phi[j * GP + g] = pf;
+      F = fmaf(c_nusf[m * kMaxG + g], pf, F);
+    }
+    fnew[j] = F;
+    acc += V * (double)F;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = acc;
+    if (bad) atomicAdd(&sc[SC_BAD], (double)bad);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+  }
+}
+
+// k update (single block): k_new = k * sum V F_new / sum V F_old; scale = 1 / sum V F_new
+__global__ void k_keff(const double* part_old, const double* part_new, int nb, double* sc) {
+  __shared__ double r1[32], r2[32];
+  double a = 0, b = 0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    a += part_old[i];
+    b += part_new[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    r1[threadIdx.x >> 5] = a;
+    r2[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a = 0;
+    b = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += r1[w];
+      b += r2[w];
+    }
+    double k = sc[SC_K];
+    sc[SC_KPREV] = k;
+    sc[SC_PROD_OLD] = a;
+    sc[SC_PROD_NEW] = b;
+    double knew = (a > 0 && b > 0) ? k * b / a : 0.0;
+    sc[SC_K] = knew;
+    double scale = b > 0 ? 1.0 / b : 0.0;
+    sc[SC_SCALE] = scale;
+    sc[SC_PSI_SCALE] = scale;
+    sc[SC_LEAK_SCALED] = sc[SC_LEAK] * scale;
+  }
+}
+
+// normalise phi (Q12) and residual partials: RMS over fissile FSRs of (F_new - F_old)/F_new
+template <int G, int GP>
+__global__ void k_normalize(int64_t J, float* phi, const float* fnew, const float* fold, const double* sc,
+                            double* part2) {
+  __shared__ double r1[32], r2[32];
+  const float scale = (float)sc[SC_SCALE];
+  double a = 0, n = 0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < J; j += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) phi[j * GP + g] *= scale;
+    float Fn = fnew[j] * scale;
+    if (Fn > 0.f) {
+      double d = ((double)Fn - (double)fold[j]) / (double)Fn;
+      a += d * d;
+      n += 1.0;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    n += __shfl_xor_sync(0xffffffffu, n, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    r1[threadIdx.x >> 5] = a;
+    r2[threadIdx.x >> 5] = n;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    a = threadIdx.x < (blockDim.x >> 5) ? r1[threadIdx.x] : 0.0;
+    n = threadIdx.x < (blockDim.x >> 5) ? r2[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      n += __shfl_xor_sync(0xffffffffu, n, o);
+    }
+    if (threadIdx.x == 0) {
+      part2[2 * blockIdx.x] = a;
+      part2[2 * blockIdx.x + 1] = n;
+    }
+  }
+}
+
+__global__ void k_resid(const double* part2, int nb, double* sc, double* hist, int hist_cap) {
+  if (threadIdx.x == 0) {
+    double a = 0, n = 0;
+    for (int i = 0; i < nb; ++i) {
+      a += part2[2 * i];
+      n += part2[2 * i + 1];
+    }
+    double r = n > 0 ? sqrt(a / n) : 0.0;
+    sc[SC_RESID] = r;
+    int it = (int)sc[SC_ITER];
+    if (it < hist_cap) {
+      hist[2 * it] = sc[SC_K];
+      hist[2 * it + 1] = r;
+    }
+    sc[SC_ITER] = it + 1;
+    sc[SC_LEAK] = 0.0;
+  }
+}
+
+__global__ void k_fill_f32(float* p, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+template <class T>
+T* dmalloc(size_t n, int64_t& bytes) {
+  T* p = nullptr;
+  if (n == 0) n = 1;
+  CUDA_OK(cudaMalloc(&p, n * sizeof(T)));
+  bytes += (int64_t)(n * sizeof(T));
+  return p;
+}
+
+}  // namespace
+
+struct moc_solver {
+  std::string err;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  moc_solver_opts opts{};
+  moc_comm_desc comm{0, 1, 0};
+  int G = 0, GP = 0, N = 0, M = 0, NL = 0, n_mat = 0;
+  int64_t J = 0, T2 = 0, S = 0, T3 = 0, N2 = 0, nseg3 = 0;
+  int64_t dev_bytes = 0;
+  double setup_ms = 0;
+  DevData dd{};
+  // device buffers
+  double *d_seg_send = nullptr, *d_planes = nullptr, *d_t_len = nullptr;
+  uint32_t* d_seg_region = nullptr;
+  int64_t* d_t_seg = nullptr;
+  int32_t* d_t_a = nullptr;
+  double *d_an_cot = nullptr, *d_an_tan = nullptr, *d_an_invsin = nullptr, *d_an_dz = nullptr, *d_an_vw = nullptr;
+  float* d_an_c = nullptr;
+  double* d_st_z0 = nullptr;
+  uint32_t* d_st_first = nullptr;
+  uint32_t* d_link = nullptr;
+  uint32_t* d_work = nullptr;
+  uint32_t nwork = 0;
+  uint32_t* d_cost = nullptr;
+  uint8_t* d_mat = nullptr;
+  float *d_qt = nullptr, *d_phi = nullptr, *d_fold = nullptr, *d_fnew = nullptr;
+  double *d_tally = nullptr, *d_vol = nullptr;
+  float* d_psi[2] = {nullptr, nullptr};
+  double *d_sc = nullptr, *d_part_a = nullptr, *d_part_b = nullptr, *d_part_c = nullptr, *d_hist = nullptr;
+  int hist_cap = 100000;
+  int cur = 0;  // psi buffer holding the incoming fluxes
+  int nb_fsr = 0, sweep_blocks = 0, sweep_threads = 256;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double sweep_ms_last = 0, iter_ms_last = 0;
+  std::vector<double> sigma_t, nusf, sigs;  // host copies (balance)
+  std::vector<int32_t> mat_host;
+  float* h_xs = nullptr;  // pinned staging for cross-section uploads
+  int64_t xs_bytes = 0;
+};
+
+namespace {
+
+void upload(const void* h, void* d, size_t bytes, cudaStream_t st) {
+  if (bytes) CUDA_OK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+}
+
+// cross-section tables -> __constant__ (padded to kMaxMat x kMaxG); the fp32 tables the
+// kernels read; sigma_t * log2(e) for the ex2-based exponential.  Pinned staging buffer
+// so the copy is truly asynchronous on the solver's stream.
+void upload_materials(moc_solver* s, const double* sigma_t, const double* sigma_s, const double* nusf,
+                      const double* chi) {
+  const int G = s->G, NM = s->n_mat;
+  if (!s->h_xs) CUDA_OK(cudaMallocHost(&s->h_xs, sizeof(float) * kMaxMat * kMaxG * (4 + kMaxG)));
+  float* t2 = s->h_xs;
+  float* t1 = t2 + kMaxMat * kMaxG;
+  float* nf = t1 + kMaxMat * kMaxG;
+  float* ch = nf + kMaxMat * kMaxG;
+  float* ss = ch + kMaxMat * kMaxG;
+  std::memset(s->h_xs, 0, sizeof(float) * kMaxMat * kMaxG * (4 + kMaxG));
+  for (int m = 0; m < NM; ++m)
+    for (int q = 0; q < G; ++q) {
+      t1[m * kMaxG + q] = (float)sigma_t[(size_t)m * G + q];
+      t2[m * kMaxG + q] = (float)(sigma_t[(size_t)m * G + q] * 1.4426950408889634);
+      nf[m * kMaxG + q] = (float)nusf[(size_t)m * G + q];
+      ch[m * kMaxG + q] = (float)chi[(size_t)m * G + q];
+      for (int h = 0; h < G; ++h) ss[(m * kMaxG + q) * kMaxG + h] = (float)sigma_s[((size_t)m * G + q) * G + h];
+    }
+  const size_t a = sizeof(float) * kMaxMat * kMaxG;
+  CUDA_OK(cudaMemcpyToSymbolAsync(c_sigt2, t2, a, 0, cudaMemcpyHostToDevice, s->stream));
+  CUDA_OK(cudaMemcpyToSymbolAsync(c_sigt, t1, a, 0, cudaMemcpyHostToDevice, s->stream));
+  CUDA_OK(cudaMemcpyToSymbolAsync(c_nusf, nf, a, 0, cudaMemcpyHostToDevice, s->stream));
+  CUDA_OK(cudaMemcpyToSymbolAsync(c_chi, ch, a, 0, cudaMemcpyHostToDevice, s->stream));
+  CUDA_OK(cudaMemcpyToSymbolAsync(c_sigs, ss, a * kMaxG, 0, cudaMemcpyHostToDevice, s->stream));
+  s->xs_bytes = (int64_t)(a * (4 + kMaxG));
+  s->sigma_t.assign(sigma_t, sigma_t + (size_t)NM * G);
+  s->nusf.assign(nusf, nusf + (size_t)NM * G);
+  s->sigs.assign(sigma_s, sigma_s + (size_t)NM * G * G);
+}
+
+template <int G, int GP>
+void run_sweep(moc_solver* s) {
+  const int in = s->cur, out = 1 - s->cur;
+  k_sweep_v1<G, GP><<<s->sweep_blocks, s->sweep_threads, 0, s->stream>>>(
+      s->dd, s->d_work, s->nwork, s->d_link, s->d_mat, s->d_qt, s->d_psi[in], s->d_psi[out], s->d_tally, s->d_sc);
+}
+
+template <int G, int GP>
+void run_iteration(moc_solver* s, bool time_it) {
+  const int nb = s->nb_fsr;
+  k_source<G, GP><<<nb, 256, 0, s->stream>>>(s->J, s->d_mat, s->d_phi, s->d_vol, s->d_sc, s->d_qt, s->d_fold,
+                                             s->d_part_a);
+  CUDA_OK(cudaMemsetAsync(s->d_tally, 0, sizeof(double) * s->J * s->GP, s->stream));
+  if (time_it) CUDA_OK(cudaEventRecord(s->ev[0], s->stream));
+  run_sweep<G, GP>(s);
+  if (time_it) CUDA_OK(cudaEventRecord(s->ev[1], s->stream));
+  k_finalize<G, GP><<<nb, 256, 0, s->stream>>>(s->J, s->d_mat, s->d_qt, s->d_tally, s->d_vol, s->d_phi, s->d_fnew,
+                                               s->d_part_b, s->d_sc);
+  k_keff<<<1, 1024, 0, s->stream>>>(s->d_part_a, s->d_part_b, nb, s->d_sc);
+  k_normalize<G, GP><<<nb, 256, 0, s->stream>>>(s->J, s->d_phi, s->d_fnew, s->d_fold, s->d_sc, s->d_part_c);
+  k_resid<<<1, 32, 0, s->stream>>>(s->d_part_c, nb, s->d_sc, s->d_hist, s->hist_cap);
+  s->cur = 1 - s->cur;
+  CUDA_OK(cudaGetLastError());
+}
+
+typedef void (*iter_fn)(moc_solver*, bool);
+iter_fn pick_iter(int G) {
+  switch (G) {
+    case 1: return run_iteration<1, 1>;
+    case 2: return run_iteration<2, 2>;
+    case 3: return run_iteration<3, 4>;
+    case 4: return run_iteration<4, 4>;
+    case 5: return run_iteration<5, 8>;
+    case 6: return run_iteration<6, 8>;
+    case 7: return run_iteration<7, 8>;
+    default: return run_iteration<8, 8>;
+  }
+}
+
+int padded_groups(int G) { return G <= 2 ? G : (G <= 4 ? 4 : 8); }
+
+void reset_state(moc_solver* s) {
+  const int nb = 1024;
+  k_fill_f32<<<nb, 256, 0, s->stream>>>(s->d_phi, s->J * s->GP, 1.0f);
+  CUDA_OK(cudaMemsetAsync(s->d_psi[0], 0, sizeof(float) * 2 * s->T3 * s->GP, s->stream));
+  CUDA_OK(cudaMemsetAsync(s->d_psi[1], 0, sizeof(float) * 2 * s->T3 * s->GP, s->stream));
+  double sc[SC_N] = {0};
+  sc[SC_K] = 1.0;
+  sc[SC_PSI_SCALE] = 1.0;
+  CUDA_OK(cudaMemcpyAsync(s->d_sc, sc, sizeof(sc), cudaMemcpyHostToDevice, s->stream));
+  CUDA_OK(cudaStreamSynchronize(s->stream));
+  s->cur = 0;
+}
+
+void destroy(moc_solver* s) {
+  if (!s) return;
+  void* ptrs[] = {s->d_seg_send, s->d_planes, s->d_t_len, s->d_seg_region, s->d_t_seg, s->d_t_a, s->d_an_cot,
+                  s->d_an_tan, s->d_an_invsin, s->d_an_dz, s->d_an_vw, s->d_an_c, s->d_st_z0, s->d_st_first,
+                  s->d_link, s->d_work, s->d_cost, s->d_mat, s->d_qt, s->d_phi, s->d_fold, s->d_fnew, s->d_tally,
+                  s->d_vol, s->d_psi[0], s->d_psi[1], s->d_sc, s->d_part_a, s->d_part_b, s->d_part_c, s->d_hist};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& e : s->ev)
+    if (e) cudaEventDestroy(e);
+  if (s->h_xs) cudaFreeHost(s->h_xs);
+}
+
+}  // namespace
+
+#define SOLVER_TRY(s, ...)                     \
+  try {                                        \
+    __VA_ARGS__;                               \
+    return MOC_OK;                             \
+  } catch (const Error& e) {                   \
+    if (s) (s)->err = e.what();                \
+    return e.code;                             \
+  } catch (const std::exception& e) {          \
+    if (s) (s)->err = e.what();                \
+    return MOC_E_INVALID_ARG;                  \
+  }
+
+extern "C" {
+
+const char* moc_solver_last_error(const moc_solver* s) { return s ? s->err.c_str() : "NULL solver"; }
+
+int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_stream, const moc_comm_desc* comm,
+                      const moc_solver_opts* opts) {
+  if (!out || !p) return MOC_E_INVALID_ARG;
+  *out = nullptr;
+  const Geometry& g = p->impl.geo;
+  const Laydown& L = p->impl.lay;
+  const Materials& mt = p->impl.mat;
+  if (!g.set || !mt.set || !L.done) {
+    p->impl.err = "solver needs materials, geometry and generated tracks";
+    return MOC_E_STATE;
+  }
+  moc_solver* s = new moc_solver();
+  auto t0 = std::chrono::steady_clock::now();
+  try {
+    if (mt.n_mat > kMaxMat) throw Error(MOC_E_PARAM, "at most 32 materials are supported");
+    if (L.n3 >= (int64_t)0x7fffffff) throw Error(MOC_E_CAPACITY, "more than 2^31 3D tracks");
+    for (size_t i = 0; i < g.material.size(); ++i)
+      if (g.material[i] >= mt.n_mat) throw Error(MOC_E_REFERENCE, "unknown material index");
+    if (opts) s->opts = *opts;
+    if (comm) s->comm = *comm;
+    s->device = device;
+    CUDA_OK(cudaSetDevice(device));
+    s->stream = (cudaStream_t)cuda_stream;
+    s->G = mt.G;
+    s->GP = padded_groups(mt.G);
+    s->N = L.N;
+    s->M = L.M;
+    s->NL = g.NL;
+    s->n_mat = mt.n_mat;
+    s->J = g.n_fsr;
+    s->T2 = L.T2();
+    s->S = L.S();
+    s->T3 = L.n3;
+    s->N2 = (int64_t)L.seg_region.size();
+    cudaStream_t st = s->stream;
+    int64_t& B = s->dev_bytes;
+    // --- laydown upload (A1/A2)
+    s->d_seg_send = dmalloc<double>(s->N2, B);
+    s->d_seg_region = dmalloc<uint32_t>(s->N2, B);
+    s->d_planes = dmalloc<double>(g.NL + 1, B);
+    s->d_t_len = dmalloc<double>(s->T2, B);
+    s->d_t_seg = dmalloc<int64_t>(s->T2 + 1, B);
+    s->d_t_a = dmalloc<int32_t>(s->T2, B);
+    const size_t AN = L.an_cot.size();
+    s->d_an_cot = dmalloc<double>(AN, B);
+    s->d_an_tan = dmalloc<double>(AN, B);
+    s->d_an_invsin = dmalloc<double>(AN, B);
+    s->d_an_dz = dmalloc<double>(AN, B);
+    s->d_an_vw = dmalloc<double>(AN, B);
+    s->d_an_c = dmalloc<float>(AN, B);
+    s->d_st_z0 = dmalloc<double>(s->S, B);
+    s->d_st_first = dmalloc<uint32_t>(s->S + 1, B);
+    upload(L.seg_send.data(), s->d_seg_send, 8 * s->N2, st);
+    upload(L.seg_region.data(), s->d_seg_region, 4 * s->N2, st);
+    upload(g.planes.data(), s->d_planes, 8 * (g.NL + 1), st);
+    upload(L.t_len.data(), s->d_t_len, 8 * s->T2, st);
+    upload(L.t_seg.data(), s->d_t_seg, 8 * (s->T2 + 1), st);
+    upload(L.t_a.data(), s->d_t_a, 4 * s->T2, st);
+    upload(L.an_cot.data(), s->d_an_cot, 8 * AN, st);
+    upload(L.an_tan.data(), s->d_an_tan, 8 * AN, st);
+    upload(L.an_invsin.data(), s->d_an_invsin, 8 * AN, st);
+    upload(L.an_dz.data(), s->d_an_dz, 8 * AN, st);
+    std::vector<double> vw(AN);
+    std::vector<float> cw(AN);
+    for (size_t u = 0; u < AN; ++u) {
+      vw[u] = L.an_w[u] / (2.0 * 3.14159265358979323846) * L.an_aperp[u];  // App. A.5
+      cw[u] = (float)(L.an_w[u] * L.an_aperp[u]);
+    }
+    upload(vw.data(), s->d_an_vw, 8 * AN, st);
+    upload(cw.data(), s->d_an_c, 4 * AN, st);
+    upload(L.st_z0.data(), s->d_st_z0, 8 * s->S, st);
+    std::vector<uint32_t> sf(s->S + 1);
+    for (int64_t q = 0; q <= s->S; ++q) sf[q] = (uint32_t)L.st_first[q];
+    upload(sf.data(), s->d_st_first, 4 * (s->S + 1), st);
+    // --- 3D links (A6)
+    {
+      std::vector<int64_t> lk(2 * s->T3);
+      links3d(g, L, lk.data());
+      std::vector<uint32_t> l32(2 * s->T3);
+      for (int64_t q = 0; q < 2 * s->T3; ++q) l32[q] = lk[q] < 0 ? 0xffffffffu : (uint32_t)lk[q];
+      s->d_link = dmalloc<uint32_t>(2 * s->T3, B);
+      upload(l32.data(), s->d_link, 4 * 2 * s->T3, st);
+      CUDA_OK(cudaStreamSynchronize(st));
+    }
+    // --- FSR arrays and materials
+    s->mat_host.resize(s->J);
+    std::vector<uint8_t> m8(s->J);
+    for (int64_t j = 0; j < s->J; ++j) {
+      s->mat_host[j] = g.mat_of_fsr(j);
+      m8[j] = (uint8_t)s->mat_host[j];
+    }
+    s->d_mat = dmalloc<uint8_t>(s->J, B);
+    upload(m8.data(), s->d_mat, s->J, st);
+    const size_t JG = (size_t)s->J * s->GP;
+    s->d_qt = dmalloc<float>(JG, B);
+    s->d_phi = dmalloc<float>(JG, B);
+    s->d_tally = dmalloc<double>(JG, B);
+    s->d_vol = dmalloc<double>(s->J, B);
+    s->d_fold = dmalloc<float>(s->J, B);
+    s->d_fnew = dmalloc<float>(s->J, B);
+    s->nb_fsr = (int)std::min<int64_t>(1184, (s->J + 255) / 256);
+    s->d_part_a = dmalloc<double>(s->nb_fsr, B);
+    s->d_part_b = dmalloc<double>(s->nb_fsr, B);
+    s->d_part_c = dmalloc<double>(2 * s->nb_fsr, B);
+    s->d_sc = dmalloc<double>(SC_N, B);
+    s->d_hist = dmalloc<double>(2 * (size_t)s->hist_cap, B);
+    upload_materials(s, mt.sigma_t.data(), mt.sigma_s.data(), mt.nu_sigma_f.data(), mt.chi.data());
+    // --- device view
+    DevData& d = s->dd;
+    d.seg_send = s->d_seg_send;
+    d.seg_region = s->d_seg_region;
+    d.planes = s->d_planes;
+    d.NL = g.NL;
+    d.Z = g.Z;
+    d.t_len = s->d_t_len;
+    d.t_seg = s->d_t_seg;
+    d.t_a = s->d_t_a;
+    d.an_cot = s->d_an_cot;
+    d.an_tan = s->d_an_tan;
+    d.an_invsin = s->d_an_invsin;
+    d.an_dz = s->d_an_dz;
+    d.an_c = s->d_an_c;
+    d.an_vw = s->d_an_vw;
+    d.st_z0 = s->d_st_z0;
+    d.st_first = s->d_st_first;
+    d.S = (int32_t)s->S;
+    d.N = s->N;
+    d.T3 = (uint32_t)s->T3;
+    // --- track volumes and exact per-track segment counts (device OTF walk)
+    s->d_cost = dmalloc<uint32_t>(s->T3, B);
+    unsigned long long* d_total = dmalloc<unsigned long long>(1, B);
+    CUDA_OK(cudaMemsetAsync(s->d_vol, 0, 8 * s->J, st));
+    CUDA_OK(cudaMemsetAsync(d_total, 0, 8, st));
+    k_volumes_costs<<<148 * 8, 256, 0, st>>>(d, s->d_vol, s->d_cost, d_total);
+    CUDA_OK(cudaGetLastError());
+    unsigned long long tot = 0;
+    CUDA_OK(cudaMemcpyAsync(&tot, d_total, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    cudaFree(d_total);
+    s->nseg3 = (int64_t)tot;
+    // --- work list (schedule)
+    s->d_work = dmalloc<uint32_t>(s->T3, B);
+    s->nwork = (uint32_t)s->T3;
+    auto pol = thrust::cuda::par.on(st);
+    thrust::sequence(pol, thrust::device_ptr<uint32_t>(s->d_work), thrust::device_ptr<uint32_t>(s->d_work) + s->T3);
+    int sched = s->opts.schedule;
+    if (sched == 0 || sched == 2) {
+      // §4.3: sort by segment count descending; schedule 2 adds the serpentine reversal
+      std::vector<uint32_t> dummy;
+      uint32_t* keys = dmalloc<uint32_t>(s->T3, B);
+      CUDA_OK(cudaMemcpyAsync(keys, s->d_cost, 4 * s->T3, cudaMemcpyDeviceToDevice, st));
+      thrust::stable_sort_by_key(pol, thrust::device_ptr<uint32_t>(keys), thrust::device_ptr<uint32_t>(keys) + s->T3,
+                                 thrust::device_ptr<uint32_t>(s->d_work), thrust::greater<uint32_t>());
+      cudaFree(keys);
+      B -= 4 * s->T3;
+      int th = s->opts.threads > 0 ? s->opts.threads : 512;
+      int bl = s->opts.blocks > 0 ? s->opts.blocks : 512;
+      if (sched == 2) {
+        k_serpentine<<<1024, 256, 0, st>>>(s->d_work, (uint64_t)s->T3, (uint64_t)th * bl);
+        CUDA_OK(cudaGetLastError());
+      }
+    }
+    if (sched == 1 || sched == 2) {
+      s->sweep_threads = s->opts.threads > 0 ? s->opts.threads : 512;  // P:146 default 512 x 512
+      s->sweep_blocks = s->opts.blocks > 0 ? s->opts.blocks : 512;
+    } else {
+      s->sweep_threads = 256;
+      s->sweep_blocks = 148 * 8;
+    }
+    // --- state
+    s->d_psi[0] = dmalloc<float>(2 * (size_t)s->T3 * s->GP, B);
+    s->d_psi[1] = dmalloc<float>(2 * (size_t)s->T3 * s->GP, B);
+    for (auto& e : s->ev) CUDA_OK(cudaEventCreate(&e));
+    reset_state(s);
+  } catch (const Error& e) {
+    p->impl.err = e.what();
+    int code = e.code;
+    destroy(s);
+    delete s;
+    return code;
+  }
+  s->setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  *out = s;
+  return MOC_OK;
+}
+
+int moc_solver_destroy(moc_solver* s) {
+  destroy(s);
+  delete s;
+  return MOC_OK;
+}
+
+int moc_reset(moc_solver* s) {
+  if (!s) return MOC_E_INVALID_ARG;
+  SOLVER_TRY(s, { reset_state(s); })
+}
+
+static void read_scalars(moc_solver* s, double* sc) {
+  CUDA_OK(cudaMemcpyAsync(sc, s->d_sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_OK(cudaStreamSynchronize(s->stream));
+}
+
+static void check_health(moc_solver* s, const double* sc) {
+  if (sc[SC_BAD] > 0) throw Error(MOC_E_NUMERIC, "NaN or negative scalar flux after the sweep");
+  if (!(sc[SC_K] > 0)) throw Error(MOC_E_EIGEN, "zero fission source (k <= 0)");
+}
+
+int moc_iterate(moc_solver* s, int32_t n_iter, double* k_out, double* residual_out) {
+  if (!s || n_iter < 0) return MOC_E_INVALID_ARG;
+  SOLVER_TRY(s, {
+    CUDA_OK(cudaSetDevice(s->device));
+    iter_fn f = pick_iter(s->G);
+    for (int it = 0; it < n_iter; ++it) {
+      bool last = it == n_iter - 1;
+      if (last) CUDA_OK(cudaEventRecord(s->ev[2], s->stream));
+      f(s, last);
+      if (last) CUDA_OK(cudaEventRecord(s->ev[3], s->stream));
+    }
+    double sc[SC_N];
+    read_scalars(s, sc);
+    if (n_iter > 0) {
+      float ms = 0;
+      CUDA_OK(cudaEventElapsedTime(&ms, s->ev[0], s->ev[1]));
+      s->sweep_ms_last = ms;
+      CUDA_OK(cudaEventElapsedTime(&ms, s->ev[2], s->ev[3]));
+      s->iter_ms_last = ms;
+    }
+    check_health(s, sc);
+    if (k_out) *k_out = sc[SC_K];
+    if (residual_out) *residual_out = sc[SC_RESID];
+  })
+}
+
+int moc_solve(moc_solver* s, const moc_solve_opts* o, moc_result* r) {
+  if (!s || !o || !r) return MOC_E_INVALID_ARG;
+  try {
+    CUDA_OK(cudaSetDevice(s->device));
+    iter_fn f = pick_iter(s->G);
+    int every = o->check_every > 0 ? o->check_every : 10;
+    int done = 0;
+    r->converged = 0;
+    while (done < o->max_iter) {
+      int n = std::min(every, o->max_iter - done);
+      for (int it = 0; it < n; ++it) f(s, false);
+      done += n;
+      double sc[SC_N];
+      read_scalars(s, sc);
+      check_health(s, sc);
+      r->k = sc[SC_K];
+      r->residual = sc[SC_RESID];
+      r->iterations = (int32_t)sc[SC_ITER];
+      // convergence on the latest iteration
+      if (std::fabs(sc[SC_K] - sc[SC_KPREV]) < o->tol_k && sc[SC_RESID] < o->tol_src) {
+        // find the first converged iteration inside the batch from the history
+        std::vector<double> h(2 * (size_t)std::min(r->iterations, s->hist_cap));
+        CUDA_OK(cudaMemcpy(h.data(), s->d_hist, 8 * h.size(), cudaMemcpyDeviceToHost));
+        r->converged = 1;
+        return MOC_OK;
+      }
+    }
+    s->err = "max_iter reached without convergence";
+    return MOC_E_NOCONV;
+  } catch (const Error& e) {
+    s->err = e.what();
+    return e.code;
+  }
+}
+
+int moc_solver_update_materials(moc_solver* s, const double* sigma_t, const double* sigma_s, const double* nu_sigma_f,
+                                const double* chi) {
+  if (!s || !sigma_t || !sigma_s || !nu_sigma_f || !chi) return MOC_E_INVALID_ARG;
+  SOLVER_TRY(s, {
+    for (int64_t q = 0; q < (int64_t)s->n_mat * s->G; ++q)
+      if (!(sigma_t[q] > 0)) throw Error(MOC_E_PARAM, "sigma_t must be > 0");
+    upload_materials(s, sigma_t, sigma_s, nu_sigma_f, chi);
+  })
+}
+
+int moc_get_scalar_flux(moc_solver* s, double* phi) {
+  if (!s || !phi) return MOC_E_INVALID_ARG;
+  SOLVER_TRY(s, {
+    std::vector<float> h((size_t)s->J * s->GP);
+    CUDA_OK(cudaMemcpyAsync(h.data(), s->d_phi, 4 * h.size(), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_OK(cudaStreamSynchronize(s->stream));
+    for (int64_t j = 0; j < s->J; ++j)
+      for (int g = 0; g < s->G; ++g) phi[j * s->G + g] = h[j * s->GP + g];
+  })
+}
+
+int moc_get_fsr_volumes(moc_solver* s, double* vol) {
+  if (!s || !vol) return MOC_E_INVALID_ARG;
+  SOLVER_TRY(s, {
+    CUDA_OK(cudaMemcpyAsync(vol, s->d_vol, 8 * s->J, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_OK(cudaStreamSynchronize(s->stream));
+  })
+}
+
+int moc_get_history(moc_solver* s, double* k_hist, double* res_hist, int32_t cap, int32_t* n) {
+  if (!s || !n) return MOC_E_INVALID_ARG;
+  SOLVER_TRY(s, {
+    double sc[SC_N];
+    read_scalars(s, sc);
+    int it = std::min((int)sc[SC_ITER], s->hist_cap);
+    std::vector<double> h(2 * (size_t)std::max(it, 1));
+    CUDA_OK(cudaMemcpy(h.data(), s->d_hist, 8 * 2 * (size_t)it, cudaMemcpyDeviceToHost));
+    int m = std::min(it, cap);
+    for (int q = 0; q < m; ++q) {
+      if (k_hist) k_hist[q] = h[2 * q];
+      if (res_hist) res_hist[q] = h[2 * q + 1];
+    }
+    *n = it;
+  })
+}
+
+int moc_get_balance(moc_solver* s, double* production, double* absorption, double* leakage) {
+  if (!s) return MOC_E_INVALID_ARG;
+  SOLVER_TRY(s, {
+    std::vector<double> phi((size_t)s->J * s->G), vol(s->J);
+    int rc = moc_get_scalar_flux(s, phi.data());
+    if (rc) throw Error(rc, s->err);
+    rc = moc_get_fsr_volumes(s, vol.data());
+    if (rc) throw Error(rc, s->err);
+    double sc[SC_N];
+    read_scalars(s, sc);
+    double pr = 0, ab = 0;
+    const int G = s->G;
+    for (int64_t j = 0; j < s->J; ++j) {
+      int m = s->mat_host[j];
+      for (int g = 0; g < G; ++g) {
+        double sa = s->sigma_t[(size_t)m * G + g];
+        for (int h = 0; h < G; ++h) sa -= s->sigs[((size_t)m * G + g) * G + h];
+        ab += vol[j] * sa * phi[(size_t)j * G + g];
+        pr += vol[j] * s->nusf[(size_t)m * G + g] * phi[(size_t)j * G + g];
+      }
+    }
+    if (production) *production = pr;
+    if (absorption) *absorption = ab;
+    if (leakage) *leakage = sc[SC_LEAK_SCALED];
+  })
+}
+
+int moc_device_trace_checksums(moc_solver* s, int64_t first, int64_t n, int32_t* nseg, uint64_t* hash, double* suml) {
+  if (!s || first < 0 || n < 0 || first + n > s->T3) return MOC_E_INVALID_ARG;
+  SOLVER_TRY(s, {
+    if (n == 0) return MOC_OK;
+    int64_t B = 0;
+    int32_t* dn = dmalloc<int32_t>(n, B);
+    unsigned long long* dh = dmalloc<unsigned long long>(n, B);
+    double* ds = dmalloc<double>(n, B);
+    k_checksums<<<(int)std::min<int64_t>(4096, (n + 255) / 256), 256, 0, s->stream>>>(s->dd, (uint32_t)first,
+                                                                                     (uint32_t)n, dn, dh, ds);
+    CUDA_OK(cudaGetLastError());
+    if (nseg) CUDA_OK(cudaMemcpyAsync(nseg, dn, 4 * n, cudaMemcpyDeviceToHost, s->stream));
+    if (hash) CUDA_OK(cudaMemcpyAsync(hash, dh, 8 * n, cudaMemcpyDeviceToHost, s->stream));
+    if (suml) CUDA_OK(cudaMemcpyAsync(suml, ds, 8 * n, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_OK(cudaStreamSynchronize(s->stream));
+    cudaFree(dn);
+    cudaFree(dh);
+    cudaFree(ds);
+  })
+}
+
+int moc_get_timings(moc_solver* s, moc_timings* t) {
+  if (!s || !t) return MOC_E_INVALID_ARG;
+  t->n_segs3d = s->nseg3;
+  t->n_integrations = 2 * s->nseg3 * s->G;
+  t->sweep_ms_last = s->sweep_ms_last;
+  t->iter_ms_last = s->iter_ms_last;
+  t->launches_per_iter = 6;  // source, sweep, finalize, keff, normalize, resid (+1 memset)
+  t->setup_ms = s->setup_ms;
+  t->device_bytes = s->dev_bytes;
+  return MOC_OK;
+}
+
+int moc_solver_comm_buffers(moc_solver* s, moc_comm_buffers* b) {
+  if (!s || !b) return MOC_E_INVALID_ARG;
+  b->tally = s->d_tally;
+  b->tally_elems = s->J * s->GP;
+  b->halo_send = nullptr;
+  b->halo_recv = nullptr;
+  b->halo_elems = 0;
+  return MOC_OK;
+}
+
+int moc_iteration_sweep(moc_solver* s) {
+  if (!s) return MOC_E_INVALID_ARG;
+  s->err = "split iterations are not implemented yet";
+  return MOC_E_STATE;
+}
+
+int moc_iteration_finish(moc_solver* s) {
+  if (!s) return MOC_E_INVALID_ARG;
+  s->err = "split iterations are not implemented yet";
+  return MOC_E_STATE;
+}
+
+}  // extern "C"
