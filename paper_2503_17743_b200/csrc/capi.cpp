@@ -260,12 +260,12 @@ int moc_trace_track_3d(const moc_problem* p, int64_t track3d, int64_t* fsr, doub
   TrackGeo tg = track_geo(p->impl.geo, L, track3d, nullptr);
   OtfView v = otf_view_host(p->impl.geo, L);
   int64_t n = 0;
-  otf_walk_fwd(v, tg, [&](int64_t, double) { ++n; });
+  otf_walk_fwd(v, tg, [&](int64_t, int, double) { ++n; });
   *nseg = n;
   if (cap < n) return MOC_E_INVALID_ARG;
   int64_t q = 0;
-  otf_walk_fwd(v, tg, [&](int64_t j, double l) {
-    if (fsr) fsr[q] = j;
+  otf_walk_fwd(v, tg, [&](int64_t k, int ly, double l) {
+    if (fsr) fsr[q] = (int64_t)v.seg_region[k] * v.NL + ly;
     if (len) len[q] = l;
     ++q;
   });
@@ -282,9 +282,9 @@ int moc_trace_track_3d_backward(const moc_problem* p, int64_t track3d, int64_t* 
   TrackGeo tg = track_geo(p->impl.geo, L, track3d, nullptr);
   OtfView v = otf_view_host(p->impl.geo, L);
   int64_t q = 0;
-  otf_walk_bwd(v, tg, [&](int64_t j, double l) {
+  otf_walk_bwd(v, tg, [&](int64_t k, int ly, double l) {
     if (q < cap) {
-      if (fsr) fsr[q] = j;
+      if (fsr) fsr[q] = (int64_t)v.seg_region[k] * v.NL + ly;
       if (len) len[q] = l;
     }
     ++q;

@@ -95,7 +95,8 @@ MOC_HD int64_t otf_seg_upto(const OtfView& v, int64_t sb, int64_t se, double s) 
   return lo;
 }
 
-// Forward walk (increasing s).  emit(int64_t fsr, double len) per merged segment.
+// Forward walk (increasing s).  emit(int64_t k, int layer, double len) per merged
+// segment: k indexes the view's 2D segment arrays, FSR j = seg_region[k] * NL + layer.
 template <class Emit>
 MOC_HD int otf_walk_fwd(const OtfView& v, const TrackGeo& g, Emit&& emit) {
   double s_in, s_out;
@@ -111,7 +112,8 @@ MOC_HD int otf_walk_fwd(const OtfView& v, const TrackGeo& g, Emit&& emit) {
     k = g.sb;
   }
   double s = s_in;
-  int64_t pj = -1;
+  int64_t pk = -1;
+  int pl = 0;
   double pL = 0.0;
   bool lead = false;
   int n = 0;
@@ -121,28 +123,30 @@ MOC_HD int otf_walk_fwd(const OtfView& v, const TrackGeo& g, Emit&& emit) {
     double s_next = s_rad < s_ax ? s_rad : s_ax;
     s_next = s_next < s_out ? s_next : s_out;
     const double L3 = (s_next - s) * g.invsin;
-    const int64_t j = (int64_t)v.seg_region[k] * v.NL + l;
-    if (pj < 0) {
-      pj = j;
+    if (pk < 0) {
+      pk = k;
+      pl = l;
       pL = L3;
       lead = L3 < kEpsL;
     } else if (L3 < kEpsL) {
       pL += L3;
     } else if (lead) {
-      pj = j;
+      pk = k;
+      pl = l;
       pL += L3;
       lead = false;
     } else {
-      emit(pj, pL);
+      emit(pk, pl, pL);
       ++n;
-      pj = j;
+      pk = k;
+      pl = l;
       pL = L3;
     }
     if (s_next >= s_out) break;
     if (s_rad <= s_ax) ++k; else l += up ? 1 : -1;
     s = s_next;
   }
-  emit(pj, pL);
+  emit(pk, pl, pL);
   return n + 1;
 }
 
@@ -163,7 +167,8 @@ MOC_HD int otf_walk_bwd(const OtfView& v, const TrackGeo& g, Emit&& emit) {
     k = g.se - 1;
   }
   double s = s_out;
-  int64_t pj = -1, last_j = -1;
+  int64_t pk = -1, lk = -1;
+  int pl = 0, ll = 0;
   double pL = 0.0, carry = 0.0;
   int n = 0;
   while (true) {
@@ -172,16 +177,17 @@ MOC_HD int otf_walk_bwd(const OtfView& v, const TrackGeo& g, Emit&& emit) {
     double s_prev = s_rad > s_ax ? s_rad : s_ax;
     s_prev = s_prev > s_in ? s_prev : s_in;
     const double L3 = (s - s_prev) * g.invsin;
-    const int64_t j = (int64_t)v.seg_region[k] * v.NL + l;
     if (L3 < kEpsL) {
       carry += L3;
-      last_j = j;
+      lk = k;
+      ll = l;
     } else {
-      if (pj >= 0) {
-        emit(pj, pL);
+      if (pk >= 0) {
+        emit(pk, pl, pL);
         ++n;
       }
-      pj = j;
+      pk = k;
+      pl = l;
       pL = L3 + carry;
       carry = 0.0;
     }
@@ -189,10 +195,10 @@ MOC_HD int otf_walk_bwd(const OtfView& v, const TrackGeo& g, Emit&& emit) {
     if (s_rad >= s_ax) --k; else l -= up ? 1 : -1;
     s = s_prev;
   }
-  if (pj >= 0) {
-    emit(pj, pL + carry);
+  if (pk >= 0) {
+    emit(pk, pl, pL + carry);
   } else {
-    emit(last_j, carry);
+    emit(lk, ll, carry);
   }
   return n + 1;
 }

@@ -126,7 +126,9 @@ __global__ void k_volumes_costs(DevData d, double* vol, uint32_t* cost, unsigned
     int s, an;
     TrackGeo g = dev_track(d, id, s, an);
     const double w = d.an_vw[an];
-    int n = otf_walk_fwd(v, g, [&](int64_t j, double len) { atomicAdd(&vol[j], w * len); });
+    int n = otf_walk_fwd(v, g, [&](int64_t k, int l, double len) {
+      atomicAdd(&vol[(int64_t)v.seg_region[k] * v.NL + l], w * len);
+    });
     cost[id] = (uint32_t)n;
     local += (unsigned long long)n;
   }
@@ -141,8 +143,8 @@ __global__ void k_checksums(DevData d, uint32_t first, uint32_t n, int32_t* nseg
     TrackGeo g = dev_track(d, first + q, s, an);
     uint64_t h = kFnvInit;
     double sl = 0;
-    int c = otf_walk_fwd(v, g, [&](int64_t j, double len) {
-      h = fnv1a_step(h, (uint32_t)j);
+    int c = otf_walk_fwd(v, g, [&](int64_t k, int l, double len) {
+      h = fnv1a_step(h, (uint32_t)((int64_t)v.seg_region[k] * v.NL + l));
       sl += len;
     });
     nseg[q] = c;
@@ -210,7 +212,7 @@ __global__ void k_source(int64_t J, const uint8_t* mat, const float* phi, const 
 // group, accumulates c * dpsi into the FSR tally with fp64 atomics (Eq. 4, Q1),
 // and writes the outgoing psi into the linked slot of the other buffer (Q9).
 template <int G, int GP>
-__global__ void __launch_bounds__(256) k_sweep_v1(DevData d, const uint32_t* work, uint32_t nwork,
+__global__ void __launch_bounds__(512) k_sweep_v1(DevData d, const uint32_t* work, uint32_t nwork,
                                                   const uint32_t* link, const uint8_t* mat, const float* qt,
                                                   const float* psi_in, float* psi_out, double* tally, double* sc) {
   const OtfView v = dev_view(d);
@@ -226,7 +228,8 @@ __global__ void __launch_bounds__(256) k_sweep_v1(DevData d, const uint32_t* wor
       float psi[G];
 #pragma unroll
       for (int q = 0; q < G; ++q) psi[q] = psi_in[(size_t)slot * GP + q] * ps;
-      auto seg = [&](int64_t j, double len) {
+      auto seg = [&](int64_t k, int l, double len) {
+        const int64_t j = (int64_t)v.seg_region[k] * v.NL + l;
         const float Lf = (float)len;
         const int m = mat[j];
 #pragma unroll
