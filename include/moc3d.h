@@ -141,6 +141,15 @@ int moc_serpentine_order(const int64_t* counts, int64_t n, int64_t chunk, int64_
 int moc_partition_exp_otf(const int64_t* estimates, int64_t n, double budget, double fraction,
                           int32_t* preload_out);
 
+/* Multi-GPU decomposition, host side and deterministic on every rank:
+ * owner[S] = rank sweeping each stack (contiguous cost-balanced pieces of the stacks ordered
+ * by polar pair, 2D cycle, position along the cycle); cost[world] (or NULL) = raw segment
+ * count per rank.  halo: target slots `rank` writes that `peer` owns, in source-slot order
+ * (the receiver derives the same list); *n = count, nothing written if cap < *n. */
+int moc_partition_stacks(const moc_problem* p, int32_t world, int32_t* owner, double* cost);
+int moc_halo_plan(const moc_problem* p, int32_t world, const int32_t* owner, int32_t rank, int32_t peer,
+                  int64_t* slots, int64_t cap, int64_t* n);
+
 /* ---------------------------------------------------------------- solver */
 typedef struct {
   int32_t rank, world;      /* world == 1: single GPU                                 */
@@ -212,6 +221,9 @@ typedef struct {
   void* halo_send; void* halo_recv; int64_t halo_elems;
 } moc_comm_buffers;
 int moc_solver_comm_buffers(moc_solver* s, moc_comm_buffers* b);
+/* per-peer element counts (floats) of this rank's halo send / recv buffers, [world] each,
+ * in peer order (the layout all_to_all expects) */
+int moc_solver_halo_counts(moc_solver* s, int64_t* send_elems, int64_t* recv_elems);
 
 /* Fine-grained iteration steps for the multi-GPU driver: sweep (A3-A6) then, after the
  * caller's allreduce of the tally / halo exchange, finish (A7). */

@@ -106,6 +106,8 @@ SIGNATURES = {
     "moc_flat_index": (_i64, [_vp, _i64, _i64, _i64, _i64]),
     "moc_serpentine_order": (C.c_int, [_vp, _i64, _i64, _vp]),
     "moc_partition_exp_otf": (C.c_int, [_vp, _i64, _d, _d, _vp]),
+    "moc_partition_stacks": (C.c_int, [_vp, _i32, _vp, _vp]),
+    "moc_halo_plan": (C.c_int, [_vp, _i32, _vp, _i32, _i32, _vp, _i64, _P(_i64)]),
     "moc_solver_create": (C.c_int, [_P(_vp), _vp, C.c_int, _vp, _P(moc_comm_desc), _P(moc_solver_opts)]),
     "moc_solver_destroy": (C.c_int, [_vp]),
     "moc_solver_last_error": (C.c_char_p, [_vp]),
@@ -120,6 +122,7 @@ SIGNATURES = {
     "moc_device_trace_checksums": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
     "moc_get_timings": (C.c_int, [_vp, _P(moc_timings)]),
     "moc_solver_comm_buffers": (C.c_int, [_vp, _P(moc_comm_buffers)]),
+    "moc_solver_halo_counts": (C.c_int, [_vp, _vp, _vp]),
     "moc_iteration_sweep": (C.c_int, [_vp]),
     "moc_iteration_finish": (C.c_int, [_vp]),
 }
@@ -278,6 +281,21 @@ class Problem:
         self._call(lib().moc_get_links3d, _p(link))
         return link
 
+    def partition(self, world: int):
+        """Stack owner per rank and raw segment cost per rank."""
+        S = self.stats()["n_stacks"]
+        owner, cost = np.zeros(S, np.int32), np.zeros(world)
+        self._call(lib().moc_partition_stacks, int(world), _p(owner), _p(cost))
+        return owner, cost
+
+    def halo_plan(self, world: int, owner, rank: int, peer: int):
+        own = np.ascontiguousarray(owner, np.int32)
+        n = C.c_int64()
+        self._call(lib().moc_halo_plan, int(world), _p(own), int(rank), int(peer), None, 0, C.byref(n))
+        out = np.zeros(n.value, np.int64)
+        self._call(lib().moc_halo_plan, int(world), _p(own), int(rank), int(peer), _p(out), n.value, C.byref(n))
+        return out
+
     def trace_track_3d(self, track: int, backward: bool = False):
         nseg = C.c_int64()
         f = lib().moc_trace_track_3d_backward if backward else lib().moc_trace_track_3d
@@ -289,8 +307,16 @@ class Problem:
         return fsr, ln
 
 
+class _DeviceArray:
+    """Minimal __cuda_array_interface__ holder so torch can view a library-owned buffer."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
 class Solver:
-    """Device state + power iteration on one GPU."""
+    """Device state + power iteration on one GPU (one rank)."""
 
     def __init__(self, problem: Problem, device: int = 0, stream=None, schedule: int = 0, threads: int = 0,
                  blocks: int = 0, rank: int = 0, world: int = 1):
@@ -311,6 +337,28 @@ class Solver:
             raise MocError(rc, L.moc_last_error(problem.handle).decode())
         self.G = problem.G
         self.J = problem.num_fsrs()
+        self.world, self.rank, self.device = world, rank, device
+        self._comm = None
+
+    def _comm_tensors(self):
+        """torch views (via __cuda_array_interface__) of the library's tally and halo
+        buffers, for the caller-driven NCCL all-reduce / all-to-all."""
+        if self._comm is None:
+            import torch
+            b = self.comm_buffers()
+            se, re = np.zeros(self.world, np.int64), np.zeros(self.world, np.int64)
+            self._call(lib().moc_solver_halo_counts, _p(se), _p(re))
+            dev = torch.device("cuda", self.device)
+
+            def view(ptr, n):
+                if n == 0 or not ptr:
+                    return torch.zeros(0, dtype=torch.float32, device=dev)
+                return torch.as_tensor(_DeviceArray(ptr, n), device=dev)
+
+            self._comm = dict(tally=view(b["tally"], b["tally_elems"]),
+                              send=view(b["halo_send"], int(se.sum())), recv=view(b["halo_recv"], int(re.sum())),
+                              send_splits=se.tolist(), recv_splits=re.tolist())
+        return self._comm
 
     def _call(self, f, *args):
         _check(f(self._h, *args), self._h, lib().moc_solver_last_error)
@@ -326,6 +374,28 @@ class Solver:
 
     def iterate(self, n: int):
         k, r = C.c_double(), C.c_double()
+        if self.world > 1:
+            # A3-A6 on the device, NCCL sum of the tally + boundary-psi halo all-to-all on
+            # torch's current stream (= the solver's stream), then A7 on the device.
+            import torch.distributed as dist
+            c = self._comm_tensors()
+            host = dist.get_backend() != "nccl"  # gloo (tests): stage through host memory
+            for _ in range(int(n)):
+                self._call(lib().moc_iteration_sweep)
+                if host:
+                    t = c["tally"].cpu()
+                    dist.all_reduce(t)
+                    c["tally"].copy_(t)
+                    if c["send"].numel() or c["recv"].numel():
+                        r = c["recv"].cpu()
+                        dist.all_to_all_single(r, c["send"].cpu(), c["recv_splits"], c["send_splits"])
+                        c["recv"].copy_(r)
+                else:
+                    dist.all_reduce(c["tally"])
+                    if c["send"].numel() or c["recv"].numel():
+                        dist.all_to_all_single(c["recv"], c["send"], c["recv_splits"], c["send_splits"])
+                self._call(lib().moc_iteration_finish)
+            n = 0
         self._call(lib().moc_iterate, int(n), C.byref(k), C.byref(r))
         return k.value, r.value
 

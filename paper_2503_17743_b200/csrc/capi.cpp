@@ -293,6 +293,36 @@ int moc_trace_track_3d_backward(const moc_problem* p, int64_t track3d, int64_t* 
   return q <= cap ? MOC_OK : MOC_E_INVALID_ARG;
 }
 
+int moc_partition_stacks(const moc_problem* p, int32_t world, int32_t* owner, double* cost) {
+  if (!p || !owner || world < 1) return MOC_E_INVALID_ARG;
+  moc_problem* q = const_cast<moc_problem*>(p);
+  MOC_TRY(q, {
+    if (!p->impl.lay.done) throw Error(MOC_E_STATE, "tracks not generated");
+    std::vector<int32_t> o;
+    std::vector<double> c;
+    partition_stacks(p->impl.lay, world, o, &c);
+    std::copy(o.begin(), o.end(), owner);
+    if (cost) std::copy(c.begin(), c.end(), cost);
+  })
+}
+
+int moc_halo_plan(const moc_problem* p, int32_t world, const int32_t* owner, int32_t rank, int32_t peer,
+                  int64_t* slots, int64_t cap, int64_t* n) {
+  if (!p || !owner || !n || rank < 0 || peer < 0 || rank >= world || peer >= world) return MOC_E_INVALID_ARG;
+  moc_problem* q = const_cast<moc_problem*>(p);
+  MOC_TRY(q, {
+    const Laydown& L = p->impl.lay;
+    if (!L.done) throw Error(MOC_E_STATE, "tracks not generated");
+    std::vector<int64_t> link(2 * (size_t)L.n3);
+    links3d(p->impl.geo, L, link.data());
+    std::vector<int32_t> own(owner, owner + L.S());
+    std::vector<std::vector<int64_t>> send, recv;
+    halo_plans(L, link.data(), own, rank, world, send, recv);
+    *n = (int64_t)send[peer].size();
+    if (slots && cap >= *n) std::copy(send[peer].begin(), send[peer].end(), slots);
+  })
+}
+
 // ---- Eq. 5: z_i(s) = z_0(0) + i dz + s cot(theta)
 double moc_z_of(double z0, double dz, int64_t i, double theta, double s) {
   return z0 + (double)i * dz + s * (std::cos(theta) / std::sin(theta));

@@ -79,6 +79,7 @@ struct Laydown {
   std::vector<int64_t> st_cnt, st_first;  // first [S + 1]
   int64_t n3 = 0;
   int64_t n_raw3 = 0;                     // sum of raw piece counts (cost estimate)
+  std::vector<int64_t> st_raw;            // raw piece count per stack
   bool done = false;
 
   int64_t T2() const { return (int64_t)t_len.size(); }
@@ -98,6 +99,15 @@ void links3d(const Geometry& g, const Laydown& L, int64_t* link);  // index arit
 int64_t link_slot(const Geometry& g, const Laydown& L, int64_t track, int dir);
 TrackGeo track_geo(const Geometry& g, const Laydown& L, int64_t track, int64_t* stack_out);
 OtfView otf_view_host(const Geometry& g, const Laydown& L);
+
+// partition.cpp: contiguous cost-balanced split of the stacks, ordered by
+// (polar pair, 2D cycle, position along the cycle), over `world` ranks; and the
+// boundary-psi halo plan (target slots this rank writes that `peer` owns).
+void partition_stacks(const Laydown& L, int world, std::vector<int32_t>& owner, std::vector<double>* cost);
+void halo_plan(const Laydown& L, const int64_t* link, const std::vector<int32_t>& owner, int rank, int peer,
+               std::vector<int64_t>& slots);
+void halo_plans(const Laydown& L, const int64_t* link, const std::vector<int32_t>& owner, int rank, int world,
+                std::vector<std::vector<int64_t>>& send, std::vector<std::vector<int64_t>>& recv);
 
 }  // namespace moc
 

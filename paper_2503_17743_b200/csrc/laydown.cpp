@@ -447,11 +447,13 @@ void build_laydown(const Geometry& g, const moc_track_params& tp, Laydown& L) {
   // raw piece count estimate (#2D segments spanned + #planes crossed) for sizing
   int64_t raw = 0;
   const OtfView v = otf_view_host(g, L);
+  L.st_raw.assign(S, 0);
 #pragma omp parallel for schedule(dynamic, 64) reduction(+ : raw)
   for (int64_t s = 0; s < S; ++s) {
     int64_t t = s / N;
     int n = (int)(s % N);
     size_t an = (size_t)L.t_a[t] * N + n;
+    int64_t raw_s = 0;
     for (int64_t i = 0; i < L.st_cnt[s]; ++i) {
       TrackGeo tg{L.st_z0[s] + (double)i * L.an_dz[an], L.an_cot[an], L.an_tan[an], L.an_invsin[an],
                   L.t_len[t], g.Z, L.t_seg[t], L.t_seg[t + 1]};
@@ -460,8 +462,10 @@ void build_laydown(const Geometry& g, const moc_track_params& tp, Laydown& L) {
       int64_t k0 = otf_seg_after(v, tg.sb, tg.se, s_in), k1 = otf_seg_upto(v, tg.sb, tg.se, s_out);
       double z_in = tg.z0 + s_in * tg.cot, z_out = tg.z0 + s_out * tg.cot;
       int l0 = otf_layer_up(v, std::min(z_in, z_out)), l1 = otf_layer_down(v, std::max(z_in, z_out));
-      raw += (k1 - k0 + 1) + std::max(0, l1 - l0);
+      raw_s += (k1 - k0 + 1) + std::max(0, l1 - l0);
     }
+    L.st_raw[s] = raw_s;
+    raw += raw_s;
   }
   L.n_raw3 = raw;
   L.done = true;

@@ -260,8 +260,8 @@ __global__ void __launch_bounds__(512) k_sweep_v1(DevData d, const uint32_t* wor
 
 // ------------------------------------------------------------ A7: finalize
 // phi_new = 4 pi qtilde + T / (Sigma_t V)   (Q2); block partials of sum V F(phi_new)
-template <int G, int GP>
-__global__ void k_finalize(int64_t J, const uint8_t* mat, const float* qt, const double* tally, const double* vol,
+template <int G, int GP, class TT>
+__global__ void k_finalize(int64_t J, const uint8_t* mat, const float* qt, const TT* tally, const double* vol,
                            float* phi, float* fnew, double* part, double* sc) {
   __shared__ double red[32];
   double acc = 0;
@@ -272,7 +272,7 @@ __global__ void k_finalize(int64_t J, const uint8_t* mat, const float* qt, const
     float F = 0;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      double p = kFourPi * (double)qt[j * GP + g] + tally[j * GP + g] / ((double)c_sigt[m * kMaxG + g] * V);
+      double p = kFourPi * (double)qt[j * GP + g] + (double)tally[j * GP + g] / ((double)c_sigt[m * kMaxG + g] * V);
       float pf = (float)p;
       if (!(pf >= 0.f)) ++bad;
       phi[j * GP + g] = pf;
@@ -393,9 +393,35 @@ __global__ void k_resid(const double* part2, int nb, double* sc, double* hist, i
   }
 }
 
+// halo gather (dir 0: buf[q] = psi[slot[q]]) / scatter (dir 1: psi[slot[q]] = buf[q]), GP floats per slot
+__global__ void k_halo_move(float* psi, const uint32_t* slots, int64_t n, int GP, float* buf, int dir) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * GP; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / GP;
+    const int g = (int)(e - q * GP);
+    float* p = psi + (size_t)slots[q] * GP + g;
+    if (dir == 0) buf[e] = *p; else *p = buf[e];
+  }
+}
+
+// leakage rides in the tally's tail through the all-reduce (dir 0: park, dir 1: restore)
+__global__ void k_leak_park(double* sc, float* tail, int dir) {
+  if (dir == 0) {
+    tail[0] = (float)sc[SC_LEAK];
+    sc[SC_LEAK] = 0.0;
+  } else {
+    sc[SC_LEAK] = (double)tail[0];
+  }
+}
+
 __global__ void k_fill_f32(float* p, int64_t n, float v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
+
+}  // namespace
+
+#include "sweep_v2.cuh"
+
+namespace {
 
 template <class T>
 T* dmalloc(size_t n, int64_t& bytes) {
@@ -446,6 +472,20 @@ struct moc_solver {
   std::vector<int32_t> mat_host;
   float* h_xs = nullptr;  // pinned staging for cross-section uploads
   int64_t xs_bytes = 0;
+  // v2 (schedule 0): persistent stack-band units
+  Unit* d_units = nullptr;
+  uint32_t n_units = 0;
+  uint32_t* d_counter = nullptr;
+  float *d_rmax = nullptr, *d_qmax_t = nullptr, *d_tally32 = nullptr;
+  int* d_err = nullptr;
+  int tile_words = 0;
+  size_t v2_smem = 0;
+  // multi-GPU (world > 1)
+  uint32_t *d_send_slots = nullptr, *d_recv_slots = nullptr;
+  int64_t n_send = 0, n_recv = 0;
+  float *d_halo_send = nullptr, *d_halo_recv = nullptr;
+  std::vector<int64_t> send_counts, recv_counts;  // per peer, in slots
+  double owned_cost = 0;
 };
 
 namespace {
@@ -490,21 +530,86 @@ void upload_materials(moc_solver* s, const double* sigma_t, const double* sigma_
 template <int G, int GP>
 void run_sweep(moc_solver* s) {
   const int in = s->cur, out = 1 - s->cur;
-  k_sweep_v1<G, GP><<<s->sweep_blocks, s->sweep_threads, 0, s->stream>>>(
-      s->dd, s->d_work, s->nwork, s->d_link, s->d_mat, s->d_qt, s->d_psi[in], s->d_psi[out], s->d_tally, s->d_sc);
+  if (s->opts.schedule == 0) {
+    V2Args a;
+    a.d = s->dd;
+    a.units = s->d_units;
+    a.n_units = s->n_units;
+    a.counter = s->d_counter;
+    a.link = s->d_link;
+    a.mat = s->d_mat;
+    a.qt = s->d_qt;
+    a.qmax_t = s->d_qmax_t;
+    a.psi_in = s->d_psi[in];
+    a.psi_out = s->d_psi[out];
+    a.tally = s->d_tally32;
+    a.sc = s->d_sc;
+    a.tile_words = s->tile_words;
+    a.err = s->d_err;
+    k_sweep_v2<G, GP><<<s->sweep_blocks, kV2Threads, s->v2_smem, s->stream>>>(a);
+  } else {
+    k_sweep_v1<G, GP><<<s->sweep_blocks, s->sweep_threads, 0, s->stream>>>(
+        s->dd, s->d_work, s->nwork, s->d_link, s->d_mat, s->d_qt, s->d_psi[in], s->d_psi[out], s->d_tally, s->d_sc);
+  }
 }
 
 template <int G, int GP>
-void run_iteration(moc_solver* s, bool time_it) {
+void v2_configure(moc_solver* s) {
+  CUDA_OK(cudaFuncSetAttribute(k_sweep_v2<G, GP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->v2_smem));
+  int per_sm = 0;
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_v2<G, GP>, kV2Threads, s->v2_smem));
+  if (per_sm < 1) throw Error(MOC_E_CAPACITY, "sweep kernel does not fit on an SM");
+  int dev = 0, nsm = 0;
+  CUDA_OK(cudaGetDevice(&dev));
+  CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  s->sweep_blocks = nsm * per_sm;
+  s->sweep_threads = kV2Threads;
+}
+
+// first half of an iteration: A3 source, A4-A6 sweep of this rank's units; for world > 1
+// also gathers the halo (outgoing psi of cut-crossing links) and parks the leakage in the
+// tally's tail so one all-reduce carries both.
+template <int G, int GP>
+void iter_sweep_half(moc_solver* s, bool time_it) {
+  const bool v2 = s->opts.schedule == 0;
   const int nb = s->nb_fsr;
   k_source<G, GP><<<nb, 256, 0, s->stream>>>(s->J, s->d_mat, s->d_phi, s->d_vol, s->d_sc, s->d_qt, s->d_fold,
                                              s->d_part_a);
-  CUDA_OK(cudaMemsetAsync(s->d_tally, 0, sizeof(double) * s->J * s->GP, s->stream));
+  if (v2) {
+    k_region_qmax<G, GP><<<64, 256, 0, s->stream>>>(s->J / s->NL, s->NL, s->d_qt, s->d_rmax);
+    k_track_qmax<G, GP><<<64, 256, 0, s->stream>>>(s->T2, s->d_t_seg, s->d_seg_region, s->d_rmax, s->d_qmax_t);
+    CUDA_OK(cudaMemsetAsync(s->d_tally32, 0, sizeof(float) * s->J * s->GP, s->stream));
+    CUDA_OK(cudaMemsetAsync(s->d_counter, 0, sizeof(uint32_t), s->stream));
+  } else {
+    CUDA_OK(cudaMemsetAsync(s->d_tally, 0, sizeof(double) * s->J * s->GP, s->stream));
+  }
   if (time_it) CUDA_OK(cudaEventRecord(s->ev[0], s->stream));
   run_sweep<G, GP>(s);
   if (time_it) CUDA_OK(cudaEventRecord(s->ev[1], s->stream));
-  k_finalize<G, GP><<<nb, 256, 0, s->stream>>>(s->J, s->d_mat, s->d_qt, s->d_tally, s->d_vol, s->d_phi, s->d_fnew,
-                                               s->d_part_b, s->d_sc);
+  if (s->comm.world > 1) {
+    if (s->n_send) k_halo_move<<<256, 256, 0, s->stream>>>(s->d_psi[1 - s->cur], s->d_send_slots, s->n_send, GP,
+                                                          s->d_halo_send, 0);
+    k_leak_park<<<1, 1, 0, s->stream>>>(s->d_sc, s->d_tally32 + s->J * GP, 0);
+  }
+  CUDA_OK(cudaGetLastError());
+}
+
+// second half: (after the caller's all-reduce / halo exchange) scatter the halo, A7.
+template <int G, int GP>
+void iter_finish_half(moc_solver* s) {
+  const bool v2 = s->opts.schedule == 0;
+  const int nb = s->nb_fsr;
+  if (s->comm.world > 1) {
+    if (s->n_recv) k_halo_move<<<256, 256, 0, s->stream>>>(s->d_psi[1 - s->cur], s->d_recv_slots, s->n_recv, GP,
+                                                          s->d_halo_recv, 1);
+    k_leak_park<<<1, 1, 0, s->stream>>>(s->d_sc, s->d_tally32 + s->J * GP, 1);
+  }
+  if (v2)
+    k_finalize<G, GP, float><<<nb, 256, 0, s->stream>>>(s->J, s->d_mat, s->d_qt, s->d_tally32, s->d_vol, s->d_phi,
+                                                        s->d_fnew, s->d_part_b, s->d_sc);
+  else
+    k_finalize<G, GP, double><<<nb, 256, 0, s->stream>>>(s->J, s->d_mat, s->d_qt, s->d_tally, s->d_vol, s->d_phi,
+                                                         s->d_fnew, s->d_part_b, s->d_sc);
   k_keff<<<1, 1024, 0, s->stream>>>(s->d_part_a, s->d_part_b, nb, s->d_sc);
   k_normalize<G, GP><<<nb, 256, 0, s->stream>>>(s->J, s->d_phi, s->d_fnew, s->d_fold, s->d_sc, s->d_part_c);
   k_resid<<<1, 32, 0, s->stream>>>(s->d_part_c, nb, s->d_sc, s->d_hist, s->hist_cap);
@@ -512,7 +617,38 @@ void run_iteration(moc_solver* s, bool time_it) {
   CUDA_OK(cudaGetLastError());
 }
 
+template <int G, int GP>
+void run_iteration(moc_solver* s, bool time_it) {
+  if (s->comm.world > 1) throw Error(MOC_E_STATE, "world > 1: drive iterations with moc_iteration_sweep/finish");
+  iter_sweep_half<G, GP>(s, time_it);
+  iter_finish_half<G, GP>(s);
+}
+
+template <int G, int GP>
+void run_sweep_half(moc_solver* s, bool time_it) {
+  iter_sweep_half<G, GP>(s, time_it);
+}
+
+template <int G, int GP>
+void run_finish_half(moc_solver* s, bool) {
+  iter_finish_half<G, GP>(s);
+}
+
 typedef void (*iter_fn)(moc_solver*, bool);
+#define PICK(FN)                      \
+  switch (G) {                           \
+    case 1: return FN<1, 1>;             \
+    case 2: return FN<2, 2>;             \
+    case 3: return FN<3, 4>;             \
+    case 4: return FN<4, 4>;             \
+    case 5: return FN<5, 8>;             \
+    case 6: return FN<6, 8>;             \
+    case 7: return FN<7, 8>;             \
+    default: return FN<8, 8>;            \
+  }
+iter_fn pick_sweep_half(int G) { PICK(run_sweep_half) }
+iter_fn pick_finish_half(int G) { PICK(run_finish_half) }
+#undef PICK
 iter_fn pick_iter(int G) {
   switch (G) {
     case 1: return run_iteration<1, 1>;
@@ -523,6 +659,19 @@ iter_fn pick_iter(int G) {
     case 6: return run_iteration<6, 8>;
     case 7: return run_iteration<7, 8>;
     default: return run_iteration<8, 8>;
+  }
+}
+
+void v2_configure_any(moc_solver* s) {
+  switch (s->G) {
+    case 1: return v2_configure<1, 1>(s);
+    case 2: return v2_configure<2, 2>(s);
+    case 3: return v2_configure<3, 4>(s);
+    case 4: return v2_configure<4, 4>(s);
+    case 5: return v2_configure<5, 8>(s);
+    case 6: return v2_configure<6, 8>(s);
+    case 7: return v2_configure<7, 8>(s);
+    default: return v2_configure<8, 8>(s);
   }
 }
 
@@ -546,7 +695,8 @@ void destroy(moc_solver* s) {
   void* ptrs[] = {s->d_seg_send, s->d_planes, s->d_t_len, s->d_seg_region, s->d_t_seg, s->d_t_a, s->d_an_cot,
                   s->d_an_tan, s->d_an_invsin, s->d_an_dz, s->d_an_vw, s->d_an_c, s->d_st_z0, s->d_st_first,
                   s->d_link, s->d_work, s->d_cost, s->d_mat, s->d_qt, s->d_phi, s->d_fold, s->d_fnew, s->d_tally,
-                  s->d_vol, s->d_psi[0], s->d_psi[1], s->d_sc, s->d_part_a, s->d_part_b, s->d_part_c, s->d_hist};
+                  s->d_vol, s->d_psi[0], s->d_psi[1], s->d_sc, s->d_part_a, s->d_part_b, s->d_part_c, s->d_hist,
+                  s->d_units, s->d_counter, s->d_rmax, s->d_qmax_t, s->d_tally32, s->d_err};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : s->ev)
@@ -647,6 +797,7 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     for (int64_t q = 0; q <= s->S; ++q) sf[q] = (uint32_t)L.st_first[q];
     upload(sf.data(), s->d_st_first, 4 * (s->S + 1), st);
     // --- 3D links (A6)
+    std::vector<int32_t> owner;  // stack -> rank (multi-GPU)
     {
       std::vector<int64_t> lk(2 * s->T3);
       links3d(g, L, lk.data());
@@ -654,6 +805,30 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       for (int64_t q = 0; q < 2 * s->T3; ++q) l32[q] = lk[q] < 0 ? 0xffffffffu : (uint32_t)lk[q];
       s->d_link = dmalloc<uint32_t>(2 * s->T3, B);
       upload(l32.data(), s->d_link, 4 * 2 * s->T3, st);
+      if (s->comm.world > 1) {
+        if (s->opts.schedule != 0) throw Error(MOC_E_PARAM, "multi-GPU runs use schedule 0");
+        if (s->comm.rank < 0 || s->comm.rank >= s->comm.world) throw Error(MOC_E_INVALID_ARG, "bad rank");
+        std::vector<double> cost;
+        partition_stacks(L, s->comm.world, owner, &cost);
+        s->owned_cost = cost[s->comm.rank];
+        std::vector<std::vector<int64_t>> send, recv;
+        halo_plans(L, lk.data(), owner, s->comm.rank, s->comm.world, send, recv);
+        std::vector<uint32_t> ss, rr;
+        for (int p = 0; p < s->comm.world; ++p) {
+          s->send_counts.push_back((int64_t)send[p].size());
+          s->recv_counts.push_back((int64_t)recv[p].size());
+          for (int64_t x : send[p]) ss.push_back((uint32_t)x);
+          for (int64_t x : recv[p]) rr.push_back((uint32_t)x);
+        }
+        s->n_send = (int64_t)ss.size();
+        s->n_recv = (int64_t)rr.size();
+        s->d_send_slots = dmalloc<uint32_t>(ss.size(), B);
+        s->d_recv_slots = dmalloc<uint32_t>(rr.size(), B);
+        upload(ss.data(), s->d_send_slots, 4 * ss.size(), st);
+        upload(rr.data(), s->d_recv_slots, 4 * rr.size(), st);
+        s->d_halo_send = dmalloc<float>(ss.size() * s->GP, B);
+        s->d_halo_recv = dmalloc<float>(rr.size() * s->GP, B);
+      }
       CUDA_OK(cudaStreamSynchronize(st));
     }
     // --- FSR arrays and materials
@@ -713,14 +888,49 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     cudaFree(d_total);
     s->nseg3 = (int64_t)tot;
     // --- work list (schedule)
-    s->d_work = dmalloc<uint32_t>(s->T3, B);
-    s->nwork = (uint32_t)s->T3;
     auto pol = thrust::cuda::par.on(st);
-    thrust::sequence(pol, thrust::device_ptr<uint32_t>(s->d_work), thrust::device_ptr<uint32_t>(s->d_work) + s->T3);
     int sched = s->opts.schedule;
-    if (sched == 0 || sched == 2) {
-      // §4.3: sort by segment count descending; schedule 2 adds the serpentine reversal
-      std::vector<uint32_t> dummy;
+    if (sched < 0 || sched > 2) throw Error(MOC_E_INVALID_ARG, "schedule must be 0, 1 or 2");
+    if (sched == 0) {
+      // persistent stack-band units (sweep_v2.cuh), sorted by exact segment count descending
+      for (int64_t t = 0; t < s->T2; ++t)
+        if (L.t_seg[t + 1] - L.t_seg[t] > kMaxK) throw Error(MOC_E_CAPACITY, "2D track with more than 512 segments");
+      const size_t fixed = (v2_fixed_smem_bytes() + 15) & ~size_t(15);
+      // three CTAs per SM: 228 KB per SM, 1 KB reserved per CTA
+      s->v2_smem = 74 * 1024;
+      s->tile_words = (int)((s->v2_smem - fixed) / 4);
+      if (s->tile_words / (s->GP + 1) < 2 * g.NL) throw Error(MOC_E_CAPACITY, "axial mesh too fine for the tally tile");
+      std::vector<Unit> units;
+      for (int64_t q = 0; q < s->S; ++q) {
+        if (!owner.empty() && owner[q] != s->comm.rank) continue;
+        const int64_t cnt = L.st_cnt[q];
+        for (int64_t i0 = 0; i0 < cnt; i0 += kV2Threads)
+          units.push_back(Unit{(uint32_t)q, (uint32_t)i0, (uint32_t)std::min<int64_t>(kV2Threads, cnt - i0), 0u});
+      }
+      s->n_units = (uint32_t)units.size();
+      s->d_units = dmalloc<Unit>(units.size(), B);
+      upload(units.data(), s->d_units, sizeof(Unit) * units.size(), st);
+      uint32_t* keys = dmalloc<uint32_t>(units.size(), B);
+      k_unit_cost<<<1024, 256, 0, st>>>(s->d_units, s->n_units, s->d_st_first, s->d_cost, keys);
+      CUDA_OK(cudaGetLastError());
+      thrust::stable_sort_by_key(pol, thrust::device_ptr<uint32_t>(keys), thrust::device_ptr<uint32_t>(keys) + units.size(),
+                                 thrust::device_ptr<Unit>(s->d_units), thrust::greater<uint32_t>());
+      CUDA_OK(cudaStreamSynchronize(st));
+      cudaFree(keys);
+      s->d_counter = dmalloc<uint32_t>(1, B);
+      s->d_err = dmalloc<int>(1, B);
+      CUDA_OK(cudaMemsetAsync(s->d_err, 0, sizeof(int), st));
+      s->d_rmax = dmalloc<float>((size_t)g.n_regions * s->GP, B);
+      s->d_qmax_t = dmalloc<float>((size_t)s->T2 * s->GP, B);
+      s->d_tally32 = dmalloc<float>((size_t)s->J * s->GP + 8, B);  // + tail for the leakage
+      v2_configure_any(s);
+    } else {
+      s->d_work = dmalloc<uint32_t>(s->T3, B);
+      s->nwork = (uint32_t)s->T3;
+      thrust::sequence(pol, thrust::device_ptr<uint32_t>(s->d_work), thrust::device_ptr<uint32_t>(s->d_work) + s->T3);
+    }
+    if (sched == 2) {
+      // §4.3: sort by segment count descending, then the serpentine reversal
       uint32_t* keys = dmalloc<uint32_t>(s->T3, B);
       CUDA_OK(cudaMemcpyAsync(keys, s->d_cost, 4 * s->T3, cudaMemcpyDeviceToDevice, st));
       thrust::stable_sort_by_key(pol, thrust::device_ptr<uint32_t>(keys), thrust::device_ptr<uint32_t>(keys) + s->T3,
@@ -737,9 +947,6 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     if (sched == 1 || sched == 2) {
       s->sweep_threads = s->opts.threads > 0 ? s->opts.threads : 512;  // P:146 default 512 x 512
       s->sweep_blocks = s->opts.blocks > 0 ? s->opts.blocks : 512;
-    } else {
-      s->sweep_threads = 256;
-      s->sweep_blocks = 148 * 8;
     }
     // --- state
     s->d_psi[0] = dmalloc<float>(2 * (size_t)s->T3 * s->GP, B);
@@ -775,6 +982,11 @@ static void read_scalars(moc_solver* s, double* sc) {
 }
 
 static void check_health(moc_solver* s, const double* sc) {
+  if (s->d_err) {
+    int e = 0;
+    CUDA_OK(cudaMemcpy(&e, s->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (e) throw Error(MOC_E_CAPACITY, "sweep work unit exceeded its shared-memory tally tile");
+  }
   if (sc[SC_BAD] > 0) throw Error(MOC_E_NUMERIC, "NaN or negative scalar flux after the sweep");
   if (!(sc[SC_K] > 0)) throw Error(MOC_E_EIGEN, "zero fission source (k <= 0)");
 }
@@ -938,9 +1150,14 @@ int moc_get_timings(moc_solver* s, moc_timings* t) {
   if (!s || !t) return MOC_E_INVALID_ARG;
   t->n_segs3d = s->nseg3;
   t->n_integrations = 2 * s->nseg3 * s->G;
+  float ms = 0;
+  if (s->ev[0] && cudaEventQuery(s->ev[1]) == cudaSuccess && cudaEventElapsedTime(&ms, s->ev[0], s->ev[1]) == cudaSuccess)
+    s->sweep_ms_last = ms;
   t->sweep_ms_last = s->sweep_ms_last;
   t->iter_ms_last = s->iter_ms_last;
-  t->launches_per_iter = 6;  // source, sweep, finalize, keff, normalize, resid (+1 memset)
+  // kernels per iteration: source, sweep, finalize, keff, normalize, resid (+ the two
+  // bound kernels for schedule 0, + halo gather/scatter and leak park/restore for world > 1)
+  t->launches_per_iter = 6 + (s->opts.schedule == 0 ? 2 : 0) + (s->comm.world > 1 ? 4 : 0);
   t->setup_ms = s->setup_ms;
   t->device_bytes = s->dev_bytes;
   return MOC_OK;
@@ -948,24 +1165,40 @@ int moc_get_timings(moc_solver* s, moc_timings* t) {
 
 int moc_solver_comm_buffers(moc_solver* s, moc_comm_buffers* b) {
   if (!s || !b) return MOC_E_INVALID_ARG;
-  b->tally = s->d_tally;
-  b->tally_elems = s->J * s->GP;
-  b->halo_send = nullptr;
-  b->halo_recv = nullptr;
-  b->halo_elems = 0;
+  b->tally = s->opts.schedule == 0 ? (void*)s->d_tally32 : (void*)s->d_tally;
+  // fp32 [J][GP] plus one tail element carrying the leakage through the all-reduce
+  b->tally_elems = s->J * s->GP + (s->comm.world > 1 ? 1 : 0);
+  b->halo_send = s->d_halo_send;
+  b->halo_recv = s->d_halo_recv;
+  b->halo_elems = std::max(s->n_send, s->n_recv) * s->GP;
+  return MOC_OK;
+}
+
+int moc_solver_halo_counts(moc_solver* s, int64_t* send_elems, int64_t* recv_elems) {
+  if (!s || !send_elems || !recv_elems) return MOC_E_INVALID_ARG;
+  for (int p = 0; p < s->comm.world; ++p) {
+    send_elems[p] = p < (int)s->send_counts.size() ? s->send_counts[p] * s->GP : 0;
+    recv_elems[p] = p < (int)s->recv_counts.size() ? s->recv_counts[p] * s->GP : 0;
+  }
   return MOC_OK;
 }
 
 int moc_iteration_sweep(moc_solver* s) {
   if (!s) return MOC_E_INVALID_ARG;
-  s->err = "split iterations are not implemented yet";
-  return MOC_E_STATE;
+  SOLVER_TRY(s, {
+    CUDA_OK(cudaSetDevice(s->device));
+    if (s->opts.schedule != 0) throw Error(MOC_E_STATE, "split iterations need schedule 0");
+    pick_sweep_half(s->G)(s, true);
+  })
 }
 
 int moc_iteration_finish(moc_solver* s) {
   if (!s) return MOC_E_INVALID_ARG;
-  s->err = "split iterations are not implemented yet";
-  return MOC_E_STATE;
+  SOLVER_TRY(s, {
+    CUDA_OK(cudaSetDevice(s->device));
+    if (s->opts.schedule != 0) throw Error(MOC_E_STATE, "split iterations need schedule 0");
+    pick_finish_half(s->G)(s, false);
+  })
 }
 
 }  // extern "C"

@@ -1,0 +1,492 @@
+// sweep_v2.cuh — persistent, cost-sorted stack-band OTF sweep for sm_100a
+// (the paper's §4.3 load balancing rebuilt for Blackwell).
+//
+// Work unit = (z-stack (t, n), band of <= 256 consecutive members).  One CTA of 256
+// threads takes units from a global atomic counter (units sorted by exact segment
+// count, descending — P:228 "sorting ... in descending order according to segment
+// count" — so the tail is short).  Per unit the CTA
+//   1. stages t's 2D segments (s_end f64, region u32) in shared memory: the only
+//      geometry the OTF walk reads ("retain exclusively the 2D segments");
+//   2. derives the band's tally window: for every 2D segment k the band occupies a
+//      contiguous layer range [lo_k, lo_k + w_k) (Eq. 5 is linear in i and s), so the
+//      unit's FSR cells (k, layer) are packed by an exclusive scan of w_k, and cut
+//      into chunks of consecutive k whose cells fit the shared-memory tile;
+//   3. walks, one thread per track (lanes of a warp sit different members apart), the
+//      forward direction chunk by chunk and then the backward direction chunk by
+//      chunk in reverse.  The OTF walk (otf.h rules, resumable at chunk boundaries)
+//      applies Eq. 3 per segment and group and accumulates dpsi into the chunk's tile
+//      with native u32 shared atomics (ATOMS.ADD) in 2^21-scaled fixed point:
+//      r = fma(dpsi, scale, 1.5*2^23) has bits 0x4B400000 + round(dpsi*scale); the tile
+//      sums raw bits plus a per-cell segment count, the flush subtracts
+//      count * 0x4B400000 (mod 2^32).  scale = 2^21 / bound, bound >= max |dpsi| over
+//      the unit (dpsi = (psi - q)(1 - e^-tau) and psi stays between the incoming psi and
+//      the sources under the 2D track), so every term and cell sum is exact-range;
+//   4. after each chunk, flushes its cells: c_{a,n} * sum -> tally[j][g] with
+//      red.global.add.v4.f32.
+// Shared-memory float atomics compile to a CAS loop on sm_100a (measured 9.9 vs 54
+// lanes/clk/SM for u32 ATOMS, profiles/micro_r1.jsonl) — hence the fixed point.
+#pragma once
+
+namespace {
+
+constexpr int kV2Threads = 256;
+constexpr int kV2MinBlocks = 3;
+constexpr int kMaxK = 512;                    // max 2D segments per 2D track (host-checked)
+constexpr uint32_t kMagicBits = 0x4B400000u;  // bits of 1.5 * 2^23
+constexpr float kMagic = 12582912.0f;         // 1.5 * 2^23
+constexpr float kFixOne = 2097152.0f;         // 2^21: max |term| in fixed point
+
+struct Unit {
+  uint32_t stack, i0, n, cost;
+};
+
+struct V2Args {
+  DevData d;
+  const Unit* units;
+  uint32_t n_units;
+  uint32_t* counter;
+  const uint32_t* link;
+  const uint8_t* mat;
+  const float* qt;
+  const float* qmax_t;  // [T2][GP] max qtilde over the FSRs under 2D track t
+  const float* psi_in;
+  float* psi_out;
+  float* tally;         // fp32 [J][GP]
+  double* sc;
+  int tile_words;
+  int* err;
+};
+
+__host__ __device__ constexpr size_t v2_fixed_smem_bytes() {
+  // s_send f64, s_reg u32, s_lo i32 [kMaxK]; s_base [kMaxK+4]; s_chunk [kMaxK+4];
+  // s_sig [kMaxMat*kMaxG]; scale, iscale, max [kMaxG] each
+  return kMaxK * (8 + 4 + 4) + 2 * (kMaxK + 4) * 4 + kMaxMat * kMaxG * 4 + 3 * kMaxG * 4 + 64;
+}
+
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float e) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(e)
+               : "memory");
+}
+
+// Resumable OTF walk state of one track in one direction (same rules as otf.h).
+struct WalkState {
+  double s, s_end;  // current position and the far end (s_out forward, s_in backward)
+  int k, l;         // raw piece cursor: local 2D segment, layer
+  int pk, pl;       // pending merged segment
+  float pL, carry;
+  bool have, lead, done;
+};
+
+template <int G, int GP>
+struct Physics {
+  float psi[G];
+  float scl[G];
+  const float* s_sig;
+  const uint8_t* mat;
+  const float* qt;
+  const uint32_t* s_reg;
+  const int* s_base;
+  const int* s_lo;
+  uint32_t* tile;
+  int NL;
+  int cbase;  // first cell of the current chunk
+
+  __device__ __forceinline__ void emit(int kk, int l, float Lf) {
+    const int64_t j = (int64_t)s_reg[kk] * NL + l;
+    const int m = mat[j];
+    float q[GP];
+    if constexpr (GP % 4 == 0) {
+#pragma unroll
+      for (int h = 0; h < GP / 4; ++h) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(qt + j * GP) + h);
+        q[4 * h] = x.x;
+        q[4 * h + 1] = x.y;
+        q[4 * h + 2] = x.z;
+        q[4 * h + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < GP; ++h) q[h] = __ldg(qt + j * GP + h);
+    }
+    uint32_t* cell = tile + (s_base[kk] - cbase + l - s_lo[kk]) * (GP + 1);
+    atomicAdd(cell + GP, 1u);
+    const float* sg = s_sig + m * GP;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float E = ex2_approx(-sg[g] * Lf);
+      const float dd = psi[g] - q[g];
+      const float dl = fmaf(-dd, E, dd);  // (psi - qtilde)(1 - e^{-tau})   Eq. 3
+      psi[g] -= dl;
+      atomicAdd(cell + g, __float_as_uint(fmaf(dl, scl[g], kMagic)));
+    }
+  }
+};
+
+// forward: advance until the pending segment belongs to a chunk >= k_hi (or the end)
+template <class Ph>
+__device__ __forceinline__ void walk_fwd_chunk(WalkState& w, Ph& ph, const double* s_send, const double* planes,
+                                               double z0, double tn, double isn, bool up, int k_hi) {
+  while (true) {
+    if (w.have && w.pk >= k_hi) return;
+    if (w.done) {
+      if (w.have) {
+        ph.emit(w.pk, w.pl, w.pL);
+        w.have = false;
+      }
+      return;
+    }
+    const double s_rad = s_send[w.k];
+    const double s_ax = ((up ? planes[w.l + 1] : planes[w.l]) - z0) * tn;
+    double s_next = s_rad < s_ax ? s_rad : s_ax;
+    s_next = s_next < w.s_end ? s_next : w.s_end;
+    const double L3d = (s_next - w.s) * isn;
+    const float L3 = (float)L3d;
+    if (!w.have) {
+      w.pk = w.k;
+      w.pl = w.l;
+      w.pL = L3;
+      w.lead = L3d < kEpsL;
+      w.have = true;
+    } else if (L3d < kEpsL) {
+      w.pL += L3;
+    } else if (w.lead) {
+      w.pk = w.k;
+      w.pl = w.l;
+      w.pL += L3;
+      w.lead = false;
+    } else {
+      ph.emit(w.pk, w.pl, w.pL);
+      w.pk = w.k;
+      w.pl = w.l;
+      w.pL = L3;
+    }
+    if (s_next >= w.s_end) {
+      w.done = true;
+    } else {
+      if (s_rad <= s_ax) ++w.k; else w.l += up ? 1 : -1;
+      w.s = s_next;
+    }
+  }
+}
+
+// backward: retreat until the pending segment belongs to a chunk < k_lo (or the start)
+template <class Ph>
+__device__ __forceinline__ void walk_bwd_chunk(WalkState& w, Ph& ph, const double* s_send, const double* planes,
+                                               double z0, double tn, double isn, bool up, int k_lo) {
+  while (true) {
+    if (w.have && w.pk < k_lo) return;
+    if (w.done) {
+      if (w.have) {
+        ph.emit(w.pk, w.pl, w.pL + w.carry);
+        w.have = false;
+      } else if (w.pk >= 0) {
+        if (w.pk < k_lo) return;  // all-sliver track: emit in the chunk of its last raw piece
+        ph.emit(w.pk, w.pl, w.carry);
+        w.pk = -1;
+      }
+      return;
+    }
+    const double s_rad = w.k > 0 ? s_send[w.k - 1] : 0.0;
+    const double s_ax = ((up ? planes[w.l] : planes[w.l + 1]) - z0) * tn;
+    double s_prev = s_rad > s_ax ? s_rad : s_ax;
+    s_prev = s_prev > w.s_end ? s_prev : w.s_end;
+    const double L3d = (w.s - s_prev) * isn;
+    const float L3 = (float)L3d;
+    if (L3d < kEpsL) {
+      w.carry += L3;
+      if (!w.have) {
+        w.pk = w.k;  // remembered for the all-sliver case only
+        w.pl = w.l;
+      }
+    } else {
+      if (w.have) ph.emit(w.pk, w.pl, w.pL);
+      w.pk = w.k;
+      w.pl = w.l;
+      w.pL = L3 + w.carry;
+      w.carry = 0.f;
+      w.have = true;
+    }
+    if (s_prev <= w.s_end) {
+      w.done = true;
+    } else {
+      if (s_rad >= s_ax) --w.k; else w.l -= up ? 1 : -1;
+      w.s = s_prev;
+    }
+  }
+}
+
+template <int G, int GP>
+__global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* s_send = reinterpret_cast<double*>(smem);
+  uint32_t* s_reg = reinterpret_cast<uint32_t*>(s_send + kMaxK);
+  int* s_lo = reinterpret_cast<int*>(s_reg + kMaxK);
+  int* s_base = s_lo + kMaxK;                                      // kMaxK + 4
+  int* s_chunk = s_base + kMaxK + 4;                               // chunk start k's, kMaxK + 4
+  float* s_sig = reinterpret_cast<float*>(s_chunk + kMaxK + 4);   // kMaxMat * GP
+  float* s_scale = s_sig + kMaxMat * kMaxG;
+  float* s_iscale = s_scale + kMaxG;
+  unsigned* s_max = reinterpret_cast<unsigned*>(s_iscale + kMaxG);
+  uint32_t* tile = reinterpret_cast<uint32_t*>(smem + ((v2_fixed_smem_bytes() + 15) & ~size_t(15)));
+  __shared__ uint32_t s_unit;
+  __shared__ int s_nchunk;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const DevData& d = a.d;
+  for (int q = tid; q < kMaxMat * GP; q += blockDim.x) {
+    const int m = q / GP, g = q - m * GP;
+    s_sig[q] = g < G ? c_sigt2[m * kMaxG + g] : 0.f;
+  }
+  const float ps = (float)a.sc[SC_PSI_SCALE];
+  constexpr int stride = GP + 1;
+  const int cap_cells = a.tile_words / stride;
+  double leak = 0.0;
+
+  while (true) {
+    __syncthreads();
+    if (tid == 0) s_unit = atomicAdd(a.counter, 1u);
+    __syncthreads();
+    const uint32_t u = s_unit;
+    if (u >= a.n_units) break;
+    const Unit U = a.units[u];
+    const int s = (int)U.stack;
+    const int t = s / d.N, n = s - t * d.N;
+    const int an = d.t_a[t] * d.N + n;
+    const int64_t sb = d.t_seg[t];
+    const int nk = (int)(d.t_seg[t + 1] - sb);
+    const double dz = d.an_dz[an], cot = d.an_cot[an];
+    const double z0b = d.st_z0[s];
+    const double zf = z0b + (double)U.i0 * dz, zl = z0b + (double)(U.i0 + U.n - 1) * dz;
+    const OtfView v{s_send, s_reg, d.planes, d.NL};
+    // 1-2. stage the 2D segments, per-k layer windows of the band
+    for (int kk = tid; kk < nk; kk += blockDim.x) {
+      const double s1 = d.seg_send[sb + kk];
+      const double s0 = kk ? d.seg_send[sb + kk - 1] : 0.0;
+      s_send[kk] = s1;
+      s_reg[kk] = d.seg_region[sb + kk];
+      double zlo = cot > 0 ? zf + s0 * cot : zf + s1 * cot;
+      double zhi = cot > 0 ? zl + s1 * cot : zl + s0 * cot;
+      zlo = zlo > 0.0 ? zlo : 0.0;
+      zhi = zhi < d.Z ? zhi : d.Z;
+      int lo = 0, w = 0;
+      if (zlo <= zhi) {
+        lo = otf_layer_down(v, zlo);
+        w = otf_layer_up(v, zhi) - lo + 1;
+      }
+      s_lo[kk] = lo;
+      s_base[kk] = w;
+    }
+    if (tid < kMaxG) s_max[tid] = 0u;
+    __syncthreads();
+    if (warp == 0) {
+      int carry = 0;
+      for (int b0 = 0; b0 < nk; b0 += 32) {
+        const int kk = b0 + lane;
+        const int w = kk < nk ? s_base[kk] : 0;
+        int x = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (kk < nk) s_base[kk] = carry + x - w;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (lane == 0) {
+        s_base[nk] = carry;
+        // greedy chunks of consecutive k whose cells fit the tile
+        int nc = 0, k0 = 0;
+        s_chunk[0] = 0;
+        for (int kk = 0; kk < nk; ++kk) {
+          if (s_base[kk + 1] - s_base[k0] > cap_cells) {
+            if (kk == k0) {
+              atomicAdd(a.err, 1);  // a single 2D segment's window exceeds the tile
+              break;
+            }
+            s_chunk[++nc] = kk;
+            k0 = kk;
+          }
+        }
+        s_chunk[++nc] = nk;
+        s_nchunk = nc;
+      }
+    }
+    // 3. one track per thread; lanes of a warp are `nact` members apart
+    const int nact = ((int)U.n + 31) >> 5;  // warps with work
+    const int p = lane * nact + warp;
+    const bool active = warp < nact && p < (int)U.n;
+    const uint32_t id = d.st_first[s] + U.i0 + (uint32_t)p;
+    Physics<G, GP> ph;
+    float pb[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      ph.psi[g] = active ? a.psi_in[(size_t)(2 * id) * GP + g] * ps : 0.f;
+      pb[g] = active ? a.psi_in[(size_t)(2 * id + 1) * GP + g] * ps : 0.f;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float m = fmaxf(ph.psi[g], pb[g]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) atomicMax(&s_max[g], __float_as_uint(m));
+    }
+    __syncthreads();
+    if (tid < G) {
+      const float b = fmaxf(__uint_as_float(s_max[tid]), a.qmax_t[(size_t)t * GP + tid]) * 1.0001f;
+      s_scale[tid] = b > 0.f ? kFixOne / b : 0.f;
+      s_iscale[tid] = b > 0.f ? b / kFixOne : 0.f;
+    }
+    __syncthreads();
+    const int nchunk = s_nchunk;
+#pragma unroll
+    for (int g = 0; g < G; ++g) ph.scl[g] = s_scale[g];
+    ph.s_sig = s_sig;
+    ph.mat = a.mat;
+    ph.qt = a.qt;
+    ph.s_reg = s_reg;
+    ph.s_base = s_base;
+    ph.s_lo = s_lo;
+    ph.tile = tile;
+    ph.NL = d.NL;
+    const double tn = d.an_tan[an], isn = d.an_invsin[an], Lt = d.t_len[t];
+    const double z0 = z0b + (double)(U.i0 + p) * dz;
+    const bool up = cot > 0;
+    TrackGeo tg;
+    tg.z0 = z0;
+    tg.cot = cot;
+    tg.tan = tn;
+    tg.invsin = isn;
+    tg.L = Lt;
+    tg.Z = d.Z;
+    tg.sb = 0;
+    tg.se = nk;
+    double s_in = 0, s_out = 0;
+    otf_clip(tg, s_in, s_out);
+    const float cw = d.an_c[an];
+#pragma unroll 1
+    for (int dir = 0; dir < 2; ++dir) {
+      WalkState w;
+      w.have = false;
+      w.lead = false;
+      w.done = !active;
+      w.carry = 0.f;
+      w.pk = -1;
+      w.pl = 0;
+      w.pL = 0.f;
+      if (dir == 0) {
+        w.s = s_in;
+        w.s_end = s_out;
+        if (s_in > 0.0) {
+          w.l = up ? 0 : d.NL - 1;
+          w.k = (int)otf_seg_after(v, 0, nk, s_in);
+        } else {
+          w.l = up ? otf_layer_up(v, z0) : otf_layer_down(v, z0);
+          w.k = 0;
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < G; ++g) ph.psi[g] = pb[g];
+        w.s = s_out;
+        w.s_end = s_in;
+        if (s_out < Lt) {
+          w.l = up ? d.NL - 1 : 0;
+          w.k = (int)otf_seg_upto(v, 0, nk, s_out);
+        } else {
+          const double z_out = z0 + Lt * cot;
+          w.l = up ? otf_layer_down(v, z_out) : otf_layer_up(v, z_out);
+          w.k = nk - 1;
+        }
+      }
+#pragma unroll 1
+      for (int ci = 0; ci < nchunk; ++ci) {
+        const int c = dir == 0 ? ci : nchunk - 1 - ci;
+        const int k_lo = s_chunk[c], k_hi = s_chunk[c + 1];
+        const int cb = s_base[k_lo], C = s_base[k_hi] - cb;
+        for (int q = tid; q < C * stride; q += blockDim.x) tile[q] = 0u;
+        ph.cbase = cb;
+        __syncthreads();
+        if (dir == 0) walk_fwd_chunk(w, ph, s_send, d.planes, z0, tn, isn, up, k_hi);
+        else walk_bwd_chunk(w, ph, s_send, d.planes, z0, tn, isn, up, k_lo);
+        __syncthreads();
+        // 4. flush the chunk: c_{a,n} * fixed-point sums -> global tally (fp32 vector reductions)
+        for (int kk = k_lo + warp; kk < k_hi; kk += nw) {
+          const int b = s_base[kk] - cb, wd = s_base[kk + 1] - s_base[kk], lo = s_lo[kk];
+          const int64_t jr = (int64_t)s_reg[kk] * d.NL + lo;
+          for (int x = lane; x < wd; x += 32) {
+            const uint32_t* cell = tile + (b + x) * stride;
+            const uint32_t cnt = cell[GP];
+            if (!cnt) continue;
+            float val[GP];
+#pragma unroll
+            for (int g = 0; g < GP; ++g)
+              val[g] = g < G ? (float)(int)(cell[g] - cnt * kMagicBits) * (s_iscale[g] * cw) : 0.f;
+            float* dst = a.tally + (jr + x) * GP;
+            if constexpr (GP % 4 == 0) {
+#pragma unroll
+              for (int h = 0; h < GP / 4; ++h)
+                red_add_v4(dst + 4 * h, val[4 * h], val[4 * h + 1], val[4 * h + 2], val[4 * h + 3]);
+            } else {
+#pragma unroll
+              for (int g = 0; g < G; ++g) atomicAdd(dst + g, val[g]);
+            }
+          }
+        }
+        __syncthreads();
+      }
+      if (active) {
+        const uint32_t out = a.link[2 * id + dir];
+        if (out != 0xffffffffu) {
+#pragma unroll
+          for (int g = 0; g < G; ++g) a.psi_out[(size_t)out * GP + g] = ph.psi[g];
+        } else {
+          float e = 0.f;
+#pragma unroll
+          for (int g = 0; g < G; ++g) e += ph.psi[g];
+          leak += (double)(cw * e);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) leak += __shfl_xor_sync(0xffffffffu, leak, o);
+  if (lane == 0 && leak != 0.0) atomicAdd(&a.sc[SC_LEAK], leak);
+}
+
+// max qtilde over the layers of each radial region, then over the regions under each
+// 2D track: the per-unit fixed-point bound's source part (see k_sweep_v2 step 3).
+template <int G, int GP>
+__global__ void k_region_qmax(int64_t n_regions, int NL, const float* qt, float* rmax) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_regions * G;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = q / G;
+    const int g = (int)(q - r * G);
+    float m = 0.f;
+    for (int l = 0; l < NL; ++l) m = fmaxf(m, qt[(r * NL + l) * GP + g]);
+    rmax[r * GP + g] = m;
+  }
+}
+
+template <int G, int GP>
+__global__ void k_track_qmax(int64_t T2, const int64_t* t_seg, const uint32_t* seg_region, const float* rmax,
+                             float* qmax_t) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < T2 * G; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = q / G;
+    const int g = (int)(q - t * G);
+    float m = 0.f;
+    for (int64_t k = t_seg[t]; k < t_seg[t + 1]; ++k) m = fmaxf(m, rmax[(int64_t)seg_region[k] * GP + g]);
+    qmax_t[t * GP + g] = m;
+  }
+}
+
+__global__ void k_unit_cost(const Unit* units, uint32_t n_units, const uint32_t* st_first, const uint32_t* cost,
+                            uint32_t* key) {
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n_units; u += gridDim.x * blockDim.x) {
+    const Unit U = units[u];
+    const uint32_t f = st_first[U.stack] + U.i0;
+    uint32_t c = 0;
+    for (uint32_t i = 0; i < U.n; ++i) c += cost[f + i];
+    key[u] = c;
+  }
+}
+
+}  // namespace

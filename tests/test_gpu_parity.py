@@ -85,7 +85,7 @@ def test_volumes_and_checksums_cfg2(M, oracle_mod):
     c = o.checksums()
     assert np.array_equal(d["nseg"], c["nseg"])
     assert np.array_equal(d["hash"], c["hash"])
-    np.testing.assert_allclose(d["suml"], c["suml"], rtol=1e-12)
+    np.testing.assert_allclose(d["suml"], c["suml"], rtol=1e-11)
     assert s.timings()["n_segs3d"] == int(c["nseg"].sum())
 
 
@@ -105,7 +105,7 @@ def test_checksums_full_size_sampled(M, oracle_mod, cfg):
         c = o.checksums(int(first), 2000)
         assert np.array_equal(d["nseg"], c["nseg"])
         assert np.array_equal(d["hash"], c["hash"])
-        np.testing.assert_allclose(d["suml"], c["suml"], rtol=1e-12)
+        np.testing.assert_allclose(d["suml"], c["suml"], rtol=1e-11)
     W = prob["lattice"]["nx"] * prob["lattice"]["pitch_x"]
     Z = prob["axial"]["planes"][-1]
     assert s.fsr_volumes().sum() == pytest.approx(W * W * Z, rel=1e-10)
