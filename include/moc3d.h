@@ -202,6 +202,12 @@ int moc_get_balance(moc_solver* s, double* production, double* absorption, doubl
 int moc_device_trace_checksums(moc_solver* s, int64_t first, int64_t n, int32_t* nseg,
                                uint64_t* hash, double* suml);
 
+/* Device probe of the sweep's Eq. 3 arithmetic: for host fp32 arrays of length n
+ * returns dpsi = (psi - q)(1 - e^{-sigma_t len}) and psi_out = psi - dpsi exactly as the sweep
+ * kernel evaluates them (ex2.approx on sigma_t log2(e) len, one FFMA).  For accuracy tests. */
+int moc_attenuation_probe(int device, int64_t n, const float* psi, const float* q, const float* sigma_t,
+                          const float* len, float* psi_out, float* dpsi);
+
 typedef struct {
   int64_t n_segs3d;          /* exact merged 3D segment count (device walk) */
   int64_t n_integrations;    /* per sweep: 2 * n_segs3d * G */

@@ -123,6 +123,7 @@ SIGNATURES = {
     "moc_get_timings": (C.c_int, [_vp, _P(moc_timings)]),
     "moc_solver_comm_buffers": (C.c_int, [_vp, _P(moc_comm_buffers)]),
     "moc_solver_halo_counts": (C.c_int, [_vp, _vp, _vp]),
+    "moc_attenuation_probe": (C.c_int, [C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "moc_iteration_sweep": (C.c_int, [_vp]),
     "moc_iteration_finish": (C.c_int, [_vp]),
 }
@@ -473,6 +474,15 @@ def moc_full_crossing_range(z0s, z0e, dz, zmin, zmax):
 def moc_flat_index(offsets, c, i, j, k):
     off = np.ascontiguousarray(offsets, np.int64)
     return int(lib().moc_flat_index(_p(off), int(c), int(i), int(j), int(k)))
+
+
+def moc_attenuation_probe(psi, q, sigma_t, length, device=0):
+    """The sweep kernel's Eq. 3 arithmetic on the device; returns (psi_out, dpsi) fp32."""
+    a = [np.ascontiguousarray(x, np.float32).ravel() for x in (psi, q, sigma_t, length)]
+    n = a[0].size
+    po, dp = np.zeros(n, np.float32), np.zeros(n, np.float32)
+    _check(lib().moc_attenuation_probe(int(device), n, *[_p(x) for x in a], _p(po), _p(dp)), None, None)
+    return po, dp
 
 
 def moc_serpentine_order(counts, chunk):

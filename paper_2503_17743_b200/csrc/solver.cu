@@ -375,11 +375,27 @@ __global__ void k_normalize(int64_t J, float* phi, const float* fnew, const floa
 }
 
 __global__ void k_resid(const double* part2, int nb, double* sc, double* hist, int hist_cap) {
+  __shared__ double r1[32], r2[32];
+  double a = 0, n = 0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    a += part2[2 * i];
+    n += part2[2 * i + 1];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    n += __shfl_xor_sync(0xffffffffu, n, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    r1[threadIdx.x >> 5] = a;
+    r2[threadIdx.x >> 5] = n;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    double a = 0, n = 0;
-    for (int i = 0; i < nb; ++i) {
-      a += part2[2 * i];
-      n += part2[2 * i + 1];
+    a = 0;
+    n = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += r1[w];
+      n += r2[w];
     }
     double r = n > 0 ? sqrt(a / n) : 0.0;
     sc[SC_RESID] = r;
@@ -468,6 +484,7 @@ struct moc_solver {
   int nb_fsr = 0, sweep_blocks = 0, sweep_threads = 256;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double sweep_ms_last = 0, iter_ms_last = 0;
+  bool sweep_timed = false;
   std::vector<double> sigma_t, nusf, sigs;  // host copies (balance)
   std::vector<int32_t> mat_host;
   float* h_xs = nullptr;  // pinned staging for cross-section uploads
@@ -585,7 +602,10 @@ void iter_sweep_half(moc_solver* s, bool time_it) {
   }
   if (time_it) CUDA_OK(cudaEventRecord(s->ev[0], s->stream));
   run_sweep<G, GP>(s);
-  if (time_it) CUDA_OK(cudaEventRecord(s->ev[1], s->stream));
+  if (time_it) {
+    CUDA_OK(cudaEventRecord(s->ev[1], s->stream));
+    s->sweep_timed = true;
+  }
   if (s->comm.world > 1) {
     if (s->n_send) k_halo_move<<<256, 256, 0, s->stream>>>(s->d_psi[1 - s->cur], s->d_send_slots, s->n_send, GP,
                                                           s->d_halo_send, 0);
@@ -612,7 +632,7 @@ void iter_finish_half(moc_solver* s) {
                                                          s->d_fnew, s->d_part_b, s->d_sc);
   k_keff<<<1, 1024, 0, s->stream>>>(s->d_part_a, s->d_part_b, nb, s->d_sc);
   k_normalize<G, GP><<<nb, 256, 0, s->stream>>>(s->J, s->d_phi, s->d_fnew, s->d_fold, s->d_sc, s->d_part_c);
-  k_resid<<<1, 32, 0, s->stream>>>(s->d_part_c, nb, s->d_sc, s->d_hist, s->hist_cap);
+  k_resid<<<1, 1024, 0, s->stream>>>(s->d_part_c, nb, s->d_sc, s->d_hist, s->hist_cap);
   s->cur = 1 - s->cur;
   CUDA_OK(cudaGetLastError());
 }
@@ -1151,8 +1171,10 @@ int moc_get_timings(moc_solver* s, moc_timings* t) {
   t->n_segs3d = s->nseg3;
   t->n_integrations = 2 * s->nseg3 * s->G;
   float ms = 0;
-  if (s->ev[0] && cudaEventQuery(s->ev[1]) == cudaSuccess && cudaEventElapsedTime(&ms, s->ev[0], s->ev[1]) == cudaSuccess)
+  if (s->sweep_timed && cudaEventSynchronize(s->ev[1]) == cudaSuccess &&
+      cudaEventElapsedTime(&ms, s->ev[0], s->ev[1]) == cudaSuccess)
     s->sweep_ms_last = ms;
+  (void)cudaGetLastError();  // never leave a query error behind for the next launch check
   t->sweep_ms_last = s->sweep_ms_last;
   t->iter_ms_last = s->iter_ms_last;
   // kernels per iteration: source, sweep, finalize, keff, normalize, resid (+ the two
@@ -1171,6 +1193,30 @@ int moc_solver_comm_buffers(moc_solver* s, moc_comm_buffers* b) {
   b->halo_send = s->d_halo_send;
   b->halo_recv = s->d_halo_recv;
   b->halo_elems = std::max(s->n_send, s->n_recv) * s->GP;
+  return MOC_OK;
+}
+
+int moc_attenuation_probe(int device, int64_t n, const float* psi, const float* q, const float* sigma_t,
+                          const float* len, float* psi_out, float* dpsi) {
+  if (n < 0 || (n > 0 && (!psi || !q || !sigma_t || !len || !psi_out || !dpsi))) return MOC_E_INVALID_ARG;
+  if (n == 0) return MOC_OK;
+  try {
+    CUDA_OK(cudaSetDevice(device));
+    int64_t B = 0;
+    float* d = dmalloc<float>(6 * (size_t)n, B);
+    const size_t b = sizeof(float) * n;
+    CUDA_OK(cudaMemcpy(d, psi, b, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(d + n, q, b, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(d + 2 * n, sigma_t, b, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(d + 3 * n, len, b, cudaMemcpyHostToDevice));
+    k_attenuation_probe<<<256, 256>>>(n, d, d + n, d + 2 * n, d + 3 * n, d + 4 * n, d + 5 * n);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpy(psi_out, d + 4 * n, b, cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(dpsi, d + 5 * n, b, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+  } catch (const Error& e) {
+    return e.code;
+  }
   return MOC_OK;
 }
 

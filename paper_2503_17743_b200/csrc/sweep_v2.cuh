@@ -68,6 +68,15 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
                : "memory");
 }
 
+// Eq. 3 for one segment and group: returns dpsi = (psi - qtilde)(1 - e^{-tau}) with
+// tau = sigma_t L evaluated as 2^{-(sigma_t log2 e) L} (ex2.approx.ftz) and the
+// difference folded into one FFMA: dpsi = d - d * E.
+__device__ __forceinline__ float attenuation_dpsi(float psi, float q, float sig_log2e, float L) {
+  const float E = ex2_approx(-sig_log2e * L);
+  const float dd = psi - q;
+  return fmaf(-dd, E, dd);
+}
+
 // Resumable OTF walk state of one track in one direction (same rules as otf.h).
 struct WalkState {
   double s, s_end;  // current position and the far end (s_out forward, s_in backward)
@@ -110,12 +119,23 @@ struct Physics {
     }
     uint32_t* cell = tile + (s_base[kk] - cbase + l - s_lo[kk]) * (GP + 1);
     atomicAdd(cell + GP, 1u);
-    const float* sg = s_sig + m * GP;
+    float sg[GP];
+    if constexpr (GP % 4 == 0) {
+#pragma unroll
+      for (int h = 0; h < GP / 4; ++h) {
+        const float4 x = reinterpret_cast<const float4*>(s_sig + m * GP)[h];
+        sg[4 * h] = x.x;
+        sg[4 * h + 1] = x.y;
+        sg[4 * h + 2] = x.z;
+        sg[4 * h + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < GP; ++h) sg[h] = s_sig[m * GP + h];
+    }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const float E = ex2_approx(-sg[g] * Lf);
-      const float dd = psi[g] - q[g];
-      const float dl = fmaf(-dd, E, dd);  // (psi - qtilde)(1 - e^{-tau})   Eq. 3
+      const float dl = attenuation_dpsi(psi[g], q[g], sg[g], Lf);  // Eq. 3
       psi[g] -= dl;
       atomicAdd(cell + g, __float_as_uint(fmaf(dl, scl[g], kMagic)));
     }
@@ -475,6 +495,16 @@ __global__ void k_track_qmax(int64_t T2, const int64_t* t_seg, const uint32_t* s
     float m = 0.f;
     for (int64_t k = t_seg[t]; k < t_seg[t + 1]; ++k) m = fmaxf(m, rmax[(int64_t)seg_region[k] * GP + g]);
     qmax_t[t * GP + g] = m;
+  }
+}
+
+// probe of the sweep's Eq. 3 arithmetic (tests: accuracy of the exponential path)
+__global__ void k_attenuation_probe(int64_t n, const float* psi, const float* q, const float* sig, const float* len,
+                                    float* psi_out, float* dpsi) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float d = attenuation_dpsi(psi[i], q[i], sig[i] * 1.4426950408889634f, len[i]);
+    dpsi[i] = d;
+    psi_out[i] = psi[i] - d;
   }
 }
 
