@@ -162,6 +162,8 @@ typedef struct {
                            2 = Alg. 2 over tracks sorted by segment count with the §4.3 serpentine */
   int32_t threads, blocks;  /* Alg. 2 launch shape (P:146 default 512 x 512); 0 = default */
   int32_t deterministic;    /* reserved (0) */
+  int32_t tile_cells;       /* schedule 0: cap on FSR cells per shared-memory tally chunk
+                               (0 = as many as fit; small values force many chunks, for tests) */
 } moc_solver_opts;
 
 /* Upload the laydown to `device`, allocate HBM state (boundary psi double buffer,

@@ -58,7 +58,7 @@ class moc_comm_desc(C.Structure):
 
 class moc_solver_opts(C.Structure):
     _fields_ = [("schedule", C.c_int32), ("threads", C.c_int32), ("blocks", C.c_int32),
-                ("deterministic", C.c_int32)]
+                ("deterministic", C.c_int32), ("tile_cells", C.c_int32)]
 
 
 class moc_solve_opts(C.Structure):
@@ -320,7 +320,7 @@ class Solver:
     """Device state + power iteration on one GPU (one rank)."""
 
     def __init__(self, problem: Problem, device: int = 0, stream=None, schedule: int = 0, threads: int = 0,
-                 blocks: int = 0, rank: int = 0, world: int = 1):
+                 blocks: int = 0, rank: int = 0, world: int = 1, tile_cells: int = 0):
         L = lib()
         self.problem = problem
         self._h = C.c_void_p()
@@ -330,7 +330,7 @@ class Solver:
                 stream = torch.cuda.current_stream(device).cuda_stream
             except Exception:  # torch without CUDA: legacy default stream
                 stream = 0
-        opts = moc_solver_opts(schedule, threads, blocks, 0)
+        opts = moc_solver_opts(schedule, threads, blocks, 0, tile_cells)
         comm = moc_comm_desc(rank, world, 0)
         rc = L.moc_solver_create(C.byref(self._h), problem.handle, device, C.c_void_p(stream), C.byref(comm),
                                  C.byref(opts))

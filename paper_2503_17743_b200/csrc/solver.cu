@@ -920,6 +920,10 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       s->v2_smem = 74 * 1024;
       s->tile_words = (int)((s->v2_smem - fixed) / 4);
       if (s->tile_words / (s->GP + 1) < 2 * g.NL) throw Error(MOC_E_CAPACITY, "axial mesh too fine for the tally tile");
+      if (s->opts.tile_cells > 0) {
+        if (s->opts.tile_cells < g.NL) throw Error(MOC_E_PARAM, "tile_cells must be >= the number of axial layers");
+        s->tile_words = std::min(s->tile_words, s->opts.tile_cells * (s->GP + 1));
+      }
       std::vector<Unit> units;
       for (int64_t q = 0; q < s->S; ++q) {
         if (!owner.empty() && owner[q] != s->comm.rank) continue;

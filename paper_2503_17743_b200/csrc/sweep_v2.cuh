@@ -199,6 +199,7 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState& w, Ph& ph, const doubl
       if (w.have) {
         ph.emit(w.pk, w.pl, w.pL + w.carry);
         w.have = false;
+        w.pk = -1;
       } else if (w.pk >= 0) {
         if (w.pk < k_lo) return;  // all-sliver track: emit in the chunk of its last raw piece
         ph.emit(w.pk, w.pl, w.carry);

@@ -62,6 +62,19 @@ def test_fixed_iteration_parity_small_lattice(M, oracle_mod, schedule):
     np.testing.assert_allclose(kh, ref["k_hist"], atol=1e-5)
 
 
+@pytest.mark.parametrize("tile_cells", [4, 9, 37])
+def test_many_chunk_tiles_parity(M, oracle_mod, tile_cells):
+    """Force tiny shared-memory tally chunks so every work unit is walked in many
+    resumable pieces (both directions): results must not depend on the chunking."""
+    prob = P.small_lattice(3, 3, 4)
+    s = M.Solver(M.Problem(prob), tile_cells=tile_cells)
+    k, _ = s.iterate(6)
+    ref = oracle_mod.Oracle(prob).solve(fixed_iters=6)
+    assert k == pytest.approx(ref["k"], abs=1e-5)
+    linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
+    assert linf < 1e-4, (linf, rel)
+
+
 def test_cfg2_converged_parity(M, oracle_mod):
     prob = P.config(2)
     s = M.Solver(M.Problem(prob))
