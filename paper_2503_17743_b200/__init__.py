@@ -388,9 +388,9 @@ class Solver:
                     dist.all_reduce(t)
                     c["tally"].copy_(t)
                     if c["send"].numel() or c["recv"].numel():
-                        r = c["recv"].cpu()
-                        dist.all_to_all_single(r, c["send"].cpu(), c["recv_splits"], c["send_splits"])
-                        c["recv"].copy_(r)
+                        rbuf = c["recv"].cpu()
+                        dist.all_to_all_single(rbuf, c["send"].cpu(), c["recv_splits"], c["send_splits"])
+                        c["recv"].copy_(rbuf)
                 else:
                     dist.all_reduce(c["tally"])
                     if c["send"].numel() or c["recv"].numel():

@@ -915,6 +915,7 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       // persistent stack-band units (sweep_v2.cuh), sorted by exact segment count descending
       for (int64_t t = 0; t < s->T2; ++t)
         if (L.t_seg[t + 1] - L.t_seg[t] > kMaxK) throw Error(MOC_E_CAPACITY, "2D track with more than 512 segments");
+      if (g.NL + 1 > kMaxPlanes) throw Error(MOC_E_CAPACITY, "more than 255 axial layers");
       const size_t fixed = (v2_fixed_smem_bytes() + 15) & ~size_t(15);
       // three CTAs per SM: 228 KB per SM, 1 KB reserved per CTA
       s->v2_smem = 74 * 1024;

@@ -57,10 +57,12 @@ struct V2Args {
   int* err;
 };
 
+constexpr int kMaxPlanes = 256;  // axial planes staged in shared memory (NL <= 255, host-checked)
+
 __host__ __device__ constexpr size_t v2_fixed_smem_bytes() {
-  // s_send f64, s_reg u32, s_lo i32 [kMaxK]; s_base [kMaxK+4]; s_chunk [kMaxK+4];
-  // s_sig [kMaxMat*kMaxG]; scale, iscale, max [kMaxG] each
-  return kMaxK * (8 + 4 + 4) + 2 * (kMaxK + 4) * 4 + kMaxMat * kMaxG * 4 + 3 * kMaxG * 4 + 64;
+  // s_send f64 [kMaxK], s_planes f64 [kMaxPlanes], s_reg u32, s_lo i32 [kMaxK];
+  // s_base [kMaxK+4]; s_chunk [kMaxK+4]; s_sig [kMaxMat*kMaxG]; scale, iscale, max [kMaxG] each
+  return kMaxK * (8 + 4 + 4) + kMaxPlanes * 8 + 2 * (kMaxK + 4) * 4 + kMaxMat * kMaxG * 4 + 3 * kMaxG * 4 + 64;
 }
 
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float e) {
@@ -99,31 +101,38 @@ struct Physics {
   uint32_t* tile;
   int NL;
   int cbase;  // first cell of the current chunk
+  // source and material of the pending merged segment, loaded when the segment became
+  // pending (one raw piece ahead of its use: hides the L1/L2 latency behind the walk)
+  float pq[GP];
+  int pm;
 
-  __device__ __forceinline__ void emit(int kk, int l, float Lf) {
+  __device__ __forceinline__ void prefetch(int kk, int l) {
     const int64_t j = (int64_t)s_reg[kk] * NL + l;
-    const int m = mat[j];
-    float q[GP];
+    pm = mat[j];
     if constexpr (GP % 4 == 0) {
 #pragma unroll
       for (int h = 0; h < GP / 4; ++h) {
         const float4 x = __ldg(reinterpret_cast<const float4*>(qt + j * GP) + h);
-        q[4 * h] = x.x;
-        q[4 * h + 1] = x.y;
-        q[4 * h + 2] = x.z;
-        q[4 * h + 3] = x.w;
+        pq[4 * h] = x.x;
+        pq[4 * h + 1] = x.y;
+        pq[4 * h + 2] = x.z;
+        pq[4 * h + 3] = x.w;
       }
     } else {
 #pragma unroll
-      for (int h = 0; h < GP; ++h) q[h] = __ldg(qt + j * GP + h);
+      for (int h = 0; h < GP; ++h) pq[h] = __ldg(qt + j * GP + h);
     }
+  }
+
+  // Eq. 3 on the pending segment (kk, l) of length Lf (its data prefetched)
+  __device__ __forceinline__ void emit(int kk, int l, float Lf) {
     uint32_t* cell = tile + (s_base[kk] - cbase + l - s_lo[kk]) * (GP + 1);
     atomicAdd(cell + GP, 1u);
     float sg[GP];
     if constexpr (GP % 4 == 0) {
 #pragma unroll
       for (int h = 0; h < GP / 4; ++h) {
-        const float4 x = reinterpret_cast<const float4*>(s_sig + m * GP)[h];
+        const float4 x = reinterpret_cast<const float4*>(s_sig + pm * GP)[h];
         sg[4 * h] = x.x;
         sg[4 * h + 1] = x.y;
         sg[4 * h + 2] = x.z;
@@ -131,11 +140,11 @@ struct Physics {
       }
     } else {
 #pragma unroll
-      for (int h = 0; h < GP; ++h) sg[h] = s_sig[m * GP + h];
+      for (int h = 0; h < GP; ++h) sg[h] = s_sig[pm * GP + h];
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const float dl = attenuation_dpsi(psi[g], q[g], sg[g], Lf);  // Eq. 3
+      const float dl = attenuation_dpsi(psi[g], pq[g], sg[g], Lf);  // Eq. 3
       psi[g] -= dl;
       atomicAdd(cell + g, __float_as_uint(fmaf(dl, scl[g], kMagic)));
     }
@@ -167,6 +176,7 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState& w, Ph& ph, const doubl
       w.pL = L3;
       w.lead = L3d < kEpsL;
       w.have = true;
+      ph.prefetch(w.pk, w.pl);
     } else if (L3d < kEpsL) {
       w.pL += L3;
     } else if (w.lead) {
@@ -174,11 +184,13 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState& w, Ph& ph, const doubl
       w.pl = w.l;
       w.pL += L3;
       w.lead = false;
+      ph.prefetch(w.pk, w.pl);
     } else {
       ph.emit(w.pk, w.pl, w.pL);
       w.pk = w.k;
       w.pl = w.l;
       w.pL = L3;
+      ph.prefetch(w.pk, w.pl);
     }
     if (s_next >= w.s_end) {
       w.done = true;
@@ -202,6 +214,7 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState& w, Ph& ph, const doubl
         w.pk = -1;
       } else if (w.pk >= 0) {
         if (w.pk < k_lo) return;  // all-sliver track: emit in the chunk of its last raw piece
+        ph.prefetch(w.pk, w.pl);
         ph.emit(w.pk, w.pl, w.carry);
         w.pk = -1;
       }
@@ -226,6 +239,7 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState& w, Ph& ph, const doubl
       w.pL = L3 + w.carry;
       w.carry = 0.f;
       w.have = true;
+      ph.prefetch(w.pk, w.pl);
     }
     if (s_prev <= w.s_end) {
       w.done = true;
@@ -240,7 +254,8 @@ template <int G, int GP>
 __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* s_send = reinterpret_cast<double*>(smem);
-  uint32_t* s_reg = reinterpret_cast<uint32_t*>(s_send + kMaxK);
+  double* s_planes = s_send + kMaxK;                               // kMaxPlanes
+  uint32_t* s_reg = reinterpret_cast<uint32_t*>(s_planes + kMaxPlanes);
   int* s_lo = reinterpret_cast<int*>(s_reg + kMaxK);
   int* s_base = s_lo + kMaxK;                                      // kMaxK + 4
   int* s_chunk = s_base + kMaxK + 4;                               // chunk start k's, kMaxK + 4
@@ -258,6 +273,9 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const int m = q / GP, g = q - m * GP;
     s_sig[q] = g < G ? c_sigt2[m * kMaxG + g] : 0.f;
   }
+  for (int q = tid; q <= d.NL; q += blockDim.x) s_planes[q] = d.planes[q];
+  // the tile starts zeroed; each flush re-zeroes exactly the cells it consumed
+  for (int q = tid; q < a.tile_words; q += blockDim.x) tile[q] = 0u;
   const float ps = (float)a.sc[SC_PSI_SCALE];
   constexpr int stride = GP + 1;
   const int cap_cells = a.tile_words / stride;
@@ -278,7 +296,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const double dz = d.an_dz[an], cot = d.an_cot[an];
     const double z0b = d.st_z0[s];
     const double zf = z0b + (double)U.i0 * dz, zl = z0b + (double)(U.i0 + U.n - 1) * dz;
-    const OtfView v{s_send, s_reg, d.planes, d.NL};
+    const OtfView v{s_send, s_reg, s_planes, d.NL};
     // 1-2. stage the 2D segments, per-k layer windows of the band
     for (int kk = tid; kk < nk; kk += blockDim.x) {
       const double s1 = d.seg_send[sb + kk];
@@ -422,25 +440,27 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
       for (int ci = 0; ci < nchunk; ++ci) {
         const int c = dir == 0 ? ci : nchunk - 1 - ci;
         const int k_lo = s_chunk[c], k_hi = s_chunk[c + 1];
-        const int cb = s_base[k_lo], C = s_base[k_hi] - cb;
-        for (int q = tid; q < C * stride; q += blockDim.x) tile[q] = 0u;
+        const int cb = s_base[k_lo];
         ph.cbase = cb;
+        if (dir == 0) walk_fwd_chunk(w, ph, s_send, s_planes, z0, tn, isn, up, k_hi);
+        else walk_bwd_chunk(w, ph, s_send, s_planes, z0, tn, isn, up, k_lo);
         __syncthreads();
-        if (dir == 0) walk_fwd_chunk(w, ph, s_send, d.planes, z0, tn, isn, up, k_hi);
-        else walk_bwd_chunk(w, ph, s_send, d.planes, z0, tn, isn, up, k_lo);
-        __syncthreads();
-        // 4. flush the chunk: c_{a,n} * fixed-point sums -> global tally (fp32 vector reductions)
+        // 4. flush the chunk: c_{a,n} * fixed-point sums -> global tally (fp32 vector
+        //    reductions), re-zeroing every consumed cell for the next chunk
         for (int kk = k_lo + warp; kk < k_hi; kk += nw) {
           const int b = s_base[kk] - cb, wd = s_base[kk + 1] - s_base[kk], lo = s_lo[kk];
           const int64_t jr = (int64_t)s_reg[kk] * d.NL + lo;
           for (int x = lane; x < wd; x += 32) {
-            const uint32_t* cell = tile + (b + x) * stride;
+            uint32_t* cell = tile + (b + x) * stride;
             const uint32_t cnt = cell[GP];
             if (!cnt) continue;
             float val[GP];
 #pragma unroll
-            for (int g = 0; g < GP; ++g)
+            for (int g = 0; g < GP; ++g) {
               val[g] = g < G ? (float)(int)(cell[g] - cnt * kMagicBits) * (s_iscale[g] * cw) : 0.f;
+              cell[g] = 0u;
+            }
+            cell[GP] = 0u;
             float* dst = a.tally + (jr + x) * GP;
             if constexpr (GP % 4 == 0) {
 #pragma unroll
