@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libmoc3d.so")
+# MOC3D_LIB selects an in-tree variant build (A/B performance runs); default is the product build
+SO_PATH = os.environ.get("MOC3D_LIB") or os.path.join(_HERE, "libmoc3d.so")
 
 MOC_OK = 0
 ERRORS = {

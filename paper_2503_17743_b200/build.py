@@ -27,22 +27,26 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile libmoc3d.so (or a variant `out` with extra -D `defines`, for A/B runs)."""
+    target = out or SO
+    if out is None and not force and not _stale():
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
-    tmp = SO + ".tmp"
-    cmd = [nvcc, ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-o", tmp,
+    tmp = target + ".tmp"
+    cmd = [nvcc, ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-o", tmp] + [f"-D{d}" for d in defines] + [
            "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off,-fno-fast-math",
            "-Xptxas", "-v" if verbose else "-O3",
            "-lgomp"] + [os.path.join(CSRC, f) for f in SOURCES]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd, cwd=HERE)
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(SO)
+    args = [a for a in sys.argv[1:] if not a.startswith("-")]
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    out = os.path.abspath(args[0]) if args else None
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=out, defines=defs))

@@ -572,6 +572,13 @@ void run_sweep(moc_solver* s) {
 
 template <int G, int GP>
 void v2_configure(moc_solver* s) {
+  // kV2MinBlocks CTAs per SM: 228 KB of shared memory per SM, 1 KB reserved per CTA;
+  // the dynamic part (the tally tile) is what the static per-unit tables leave.
+  cudaFuncAttributes fa{};
+  CUDA_OK(cudaFuncGetAttributes(&fa, k_sweep_v2<G, GP>));
+  const size_t per_cta = (228 * 1024) / kV2MinBlocks - 1024;
+  s->v2_smem = (per_cta - fa.sharedSizeBytes) & ~size_t(15);
+  s->tile_words = (int)(s->v2_smem / 4);
   CUDA_OK(cudaFuncSetAttribute(k_sweep_v2<G, GP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->v2_smem));
   int per_sm = 0;
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_v2<G, GP>, kV2Threads, s->v2_smem));
@@ -916,10 +923,7 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       for (int64_t t = 0; t < s->T2; ++t)
         if (L.t_seg[t + 1] - L.t_seg[t] > kMaxK) throw Error(MOC_E_CAPACITY, "2D track with more than 512 segments");
       if (g.NL + 1 > kMaxPlanes) throw Error(MOC_E_CAPACITY, "more than 255 axial layers");
-      const size_t fixed = (v2_fixed_smem_bytes() + 15) & ~size_t(15);
-      // three CTAs per SM: 228 KB per SM, 1 KB reserved per CTA
-      s->v2_smem = 74 * 1024;
-      s->tile_words = (int)((s->v2_smem - fixed) / 4);
+      v2_configure_any(s);  // tile size from the kernel's static shared footprint
       if (s->tile_words / (s->GP + 1) < 2 * g.NL) throw Error(MOC_E_CAPACITY, "axial mesh too fine for the tally tile");
       if (s->opts.tile_cells > 0) {
         if (s->opts.tile_cells < g.NL) throw Error(MOC_E_PARAM, "tile_cells must be >= the number of axial layers");
@@ -948,7 +952,6 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       s->d_rmax = dmalloc<float>((size_t)g.n_regions * s->GP, B);
       s->d_qmax_t = dmalloc<float>((size_t)s->T2 * s->GP, B);
       s->d_tally32 = dmalloc<float>((size_t)s->J * s->GP + 8, B);  // + tail for the leakage
-      v2_configure_any(s);
     } else {
       s->d_work = dmalloc<uint32_t>(s->T3, B);
       s->nwork = (uint32_t)s->T3;

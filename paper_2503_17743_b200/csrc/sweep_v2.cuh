@@ -22,19 +22,38 @@
 //      the unit (dpsi = (psi - q)(1 - e^-tau) and psi stays between the incoming psi and
 //      the sources under the 2D track), so every term and cell sum is exact-range;
 //   4. after each chunk, flushes its cells: c_{a,n} * sum -> tally[j][g] with
-//      red.global.add.v4.f32.
+//      red.global.add.v4.f32, re-zeroing them for the next chunk.
 // Shared-memory float atomics compile to a CAS loop on sm_100a (measured 9.9 vs 54
 // lanes/clk/SM for u32 ATOMS, profiles/micro_r1.jsonl) — hence the fixed point.
+// Per-unit tables live in static shared arrays (compile-time addresses); the tile is
+// the dynamic shared allocation.
 #pragma once
 
 namespace {
 
+#ifndef MOC_V2_CTAS_PER_SM
+#define MOC_V2_CTAS_PER_SM 3
+#endif
 constexpr int kV2Threads = 256;
-constexpr int kV2MinBlocks = 3;
+constexpr int kV2MinBlocks = MOC_V2_CTAS_PER_SM;  // CTAs per SM the register/smem budget targets
 constexpr int kMaxK = 512;                    // max 2D segments per 2D track (host-checked)
+constexpr int kMaxPlanes = 256;               // axial planes staged in shared memory (host-checked)
 constexpr uint32_t kMagicBits = 0x4B400000u;  // bits of 1.5 * 2^23
 constexpr float kMagic = 12582912.0f;         // 1.5 * 2^23
 constexpr float kFixOne = 2097152.0f;         // 2^21: max |term| in fixed point
+
+// per-unit shared tables
+__shared__ double sh_send[kMaxK];        // cumulative 2D segment ends of the unit's 2D track
+__shared__ double sh_planes[kMaxPlanes]; // axial planes
+__shared__ int2 sh_kinfo[kMaxK];         // {region * NL, first tile cell of k - lo_k}
+__shared__ uint32_t sh_reg[kMaxK];
+__shared__ int sh_lo[kMaxK];
+__shared__ int sh_base[kMaxK + 4];
+__shared__ int sh_chunk[kMaxK + 4];
+__shared__ __align__(16) float sh_sig[kMaxMat * kMaxG];  // sigma_t * log2(e), [m][GP]
+__shared__ float sh_iscale[kMaxG];
+__shared__ float sh_scale[kMaxG];
+__shared__ unsigned sh_max[kMaxG];
 
 struct Unit {
   uint32_t stack, i0, n, cost;
@@ -56,14 +75,6 @@ struct V2Args {
   int tile_words;
   int* err;
 };
-
-constexpr int kMaxPlanes = 256;  // axial planes staged in shared memory (NL <= 255, host-checked)
-
-__host__ __device__ constexpr size_t v2_fixed_smem_bytes() {
-  // s_send f64 [kMaxK], s_planes f64 [kMaxPlanes], s_reg u32, s_lo i32 [kMaxK];
-  // s_base [kMaxK+4]; s_chunk [kMaxK+4]; s_sig [kMaxMat*kMaxG]; scale, iscale, max [kMaxG] each
-  return kMaxK * (8 + 4 + 4) + kMaxPlanes * 8 + 2 * (kMaxK + 4) * 4 + kMaxMat * kMaxG * 4 + 3 * kMaxG * 4 + 64;
-}
 
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float e) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(e)
@@ -92,14 +103,9 @@ template <int G, int GP>
 struct Physics {
   float psi[G];
   float scl[G];
-  const float* s_sig;
   const uint8_t* mat;
   const float* qt;
-  const uint32_t* s_reg;
-  const int* s_base;
-  const int* s_lo;
   uint32_t* tile;
-  int NL;
   int cbase;  // first cell of the current chunk
   // source and material of the pending merged segment, loaded when the segment became
   // pending (one raw piece ahead of its use: hides the L1/L2 latency behind the walk)
@@ -107,7 +113,7 @@ struct Physics {
   int pm;
 
   __device__ __forceinline__ void prefetch(int kk, int l) {
-    const int64_t j = (int64_t)s_reg[kk] * NL + l;
+    const int64_t j = (int64_t)(sh_kinfo[kk].x + l);
     pm = mat[j];
     if constexpr (GP % 4 == 0) {
 #pragma unroll
@@ -126,13 +132,13 @@ struct Physics {
 
   // Eq. 3 on the pending segment (kk, l) of length Lf (its data prefetched)
   __device__ __forceinline__ void emit(int kk, int l, float Lf) {
-    uint32_t* cell = tile + (s_base[kk] - cbase + l - s_lo[kk]) * (GP + 1);
+    uint32_t* cell = tile + (sh_kinfo[kk].y - cbase + l) * (GP + 1);
     atomicAdd(cell + GP, 1u);
     float sg[GP];
     if constexpr (GP % 4 == 0) {
 #pragma unroll
       for (int h = 0; h < GP / 4; ++h) {
-        const float4 x = reinterpret_cast<const float4*>(s_sig + pm * GP)[h];
+        const float4 x = reinterpret_cast<const float4*>(sh_sig + pm * GP)[h];
         sg[4 * h] = x.x;
         sg[4 * h + 1] = x.y;
         sg[4 * h + 2] = x.z;
@@ -140,7 +146,7 @@ struct Physics {
       }
     } else {
 #pragma unroll
-      for (int h = 0; h < GP; ++h) sg[h] = s_sig[pm * GP + h];
+      for (int h = 0; h < GP; ++h) sg[h] = sh_sig[pm * GP + h];
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -153,8 +159,8 @@ struct Physics {
 
 // forward: advance until the pending segment belongs to a chunk >= k_hi (or the end)
 template <class Ph>
-__device__ __forceinline__ void walk_fwd_chunk(WalkState& w, Ph& ph, const double* s_send, const double* planes,
-                                               double z0, double tn, double isn, bool up, int k_hi) {
+__device__ __forceinline__ void walk_fwd_chunk(WalkState& w, Ph& ph, double z0, double tn, double isn, bool up,
+                                               int k_hi) {
   while (true) {
     if (w.have && w.pk >= k_hi) return;
     if (w.done) {
@@ -164,32 +170,30 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState& w, Ph& ph, const doubl
       }
       return;
     }
-    const double s_rad = s_send[w.k];
-    const double s_ax = ((up ? planes[w.l + 1] : planes[w.l]) - z0) * tn;
+    const double s_rad = sh_send[w.k];
+    const double s_ax = (sh_planes[up ? w.l + 1 : w.l] - z0) * tn;
     double s_next = s_rad < s_ax ? s_rad : s_ax;
     s_next = s_next < w.s_end ? s_next : w.s_end;
     const double L3d = (s_next - w.s) * isn;
     const float L3 = (float)L3d;
-    if (!w.have) {
-      w.pk = w.k;
-      w.pl = w.l;
-      w.pL = L3;
-      w.lead = L3d < kEpsL;
-      w.have = true;
-      ph.prefetch(w.pk, w.pl);
-    } else if (L3d < kEpsL) {
-      w.pL += L3;
-    } else if (w.lead) {
-      w.pk = w.k;
-      w.pl = w.l;
-      w.pL += L3;
-      w.lead = false;
-      ph.prefetch(w.pk, w.pl);
+    if (L3d < kEpsL) {
+      if (w.have) {
+        w.pL += L3;
+      } else {
+        w.pk = w.k;
+        w.pl = w.l;
+        w.pL = L3;
+        w.lead = true;
+        w.have = true;
+        ph.prefetch(w.pk, w.pl);
+      }
     } else {
-      ph.emit(w.pk, w.pl, w.pL);
+      if (w.have && !w.lead) ph.emit(w.pk, w.pl, w.pL);
+      w.pL = (w.have && w.lead) ? w.pL + L3 : L3;  // a leading sliver run merges forward
       w.pk = w.k;
       w.pl = w.l;
-      w.pL = L3;
+      w.lead = false;
+      w.have = true;
       ph.prefetch(w.pk, w.pl);
     }
     if (s_next >= w.s_end) {
@@ -203,8 +207,8 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState& w, Ph& ph, const doubl
 
 // backward: retreat until the pending segment belongs to a chunk < k_lo (or the start)
 template <class Ph>
-__device__ __forceinline__ void walk_bwd_chunk(WalkState& w, Ph& ph, const double* s_send, const double* planes,
-                                               double z0, double tn, double isn, bool up, int k_lo) {
+__device__ __forceinline__ void walk_bwd_chunk(WalkState& w, Ph& ph, double z0, double tn, double isn, bool up,
+                                               int k_lo) {
   while (true) {
     if (w.have && w.pk < k_lo) return;
     if (w.done) {
@@ -220,8 +224,8 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState& w, Ph& ph, const doubl
       }
       return;
     }
-    const double s_rad = w.k > 0 ? s_send[w.k - 1] : 0.0;
-    const double s_ax = ((up ? planes[w.l] : planes[w.l + 1]) - z0) * tn;
+    const double s_rad = w.k > 0 ? sh_send[w.k - 1] : 0.0;
+    const double s_ax = (sh_planes[up ? w.l : w.l + 1] - z0) * tn;
     double s_prev = s_rad > s_ax ? s_rad : s_ax;
     s_prev = s_prev > w.s_end ? s_prev : w.s_end;
     const double L3d = (w.s - s_prev) * isn;
@@ -252,18 +256,7 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState& w, Ph& ph, const doubl
 
 template <int G, int GP>
 __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* s_send = reinterpret_cast<double*>(smem);
-  double* s_planes = s_send + kMaxK;                               // kMaxPlanes
-  uint32_t* s_reg = reinterpret_cast<uint32_t*>(s_planes + kMaxPlanes);
-  int* s_lo = reinterpret_cast<int*>(s_reg + kMaxK);
-  int* s_base = s_lo + kMaxK;                                      // kMaxK + 4
-  int* s_chunk = s_base + kMaxK + 4;                               // chunk start k's, kMaxK + 4
-  float* s_sig = reinterpret_cast<float*>(s_chunk + kMaxK + 4);   // kMaxMat * GP
-  float* s_scale = s_sig + kMaxMat * kMaxG;
-  float* s_iscale = s_scale + kMaxG;
-  unsigned* s_max = reinterpret_cast<unsigned*>(s_iscale + kMaxG);
-  uint32_t* tile = reinterpret_cast<uint32_t*>(smem + ((v2_fixed_smem_bytes() + 15) & ~size_t(15)));
+  extern __shared__ __align__(16) uint32_t tile[];
   __shared__ uint32_t s_unit;
   __shared__ int s_nchunk;
 
@@ -271,9 +264,9 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
   const DevData& d = a.d;
   for (int q = tid; q < kMaxMat * GP; q += blockDim.x) {
     const int m = q / GP, g = q - m * GP;
-    s_sig[q] = g < G ? c_sigt2[m * kMaxG + g] : 0.f;
+    sh_sig[q] = g < G ? c_sigt2[m * kMaxG + g] : 0.f;
   }
-  for (int q = tid; q <= d.NL; q += blockDim.x) s_planes[q] = d.planes[q];
+  for (int q = tid; q <= d.NL; q += blockDim.x) sh_planes[q] = d.planes[q];
   // the tile starts zeroed; each flush re-zeroes exactly the cells it consumed
   for (int q = tid; q < a.tile_words; q += blockDim.x) tile[q] = 0u;
   const float ps = (float)a.sc[SC_PSI_SCALE];
@@ -296,13 +289,13 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const double dz = d.an_dz[an], cot = d.an_cot[an];
     const double z0b = d.st_z0[s];
     const double zf = z0b + (double)U.i0 * dz, zl = z0b + (double)(U.i0 + U.n - 1) * dz;
-    const OtfView v{s_send, s_reg, s_planes, d.NL};
+    const OtfView v{sh_send, sh_reg, sh_planes, d.NL};
     // 1-2. stage the 2D segments, per-k layer windows of the band
     for (int kk = tid; kk < nk; kk += blockDim.x) {
       const double s1 = d.seg_send[sb + kk];
       const double s0 = kk ? d.seg_send[sb + kk - 1] : 0.0;
-      s_send[kk] = s1;
-      s_reg[kk] = d.seg_region[sb + kk];
+      sh_send[kk] = s1;
+      sh_reg[kk] = d.seg_region[sb + kk];
       double zlo = cot > 0 ? zf + s0 * cot : zf + s1 * cot;
       double zhi = cot > 0 ? zl + s1 * cot : zl + s0 * cot;
       zlo = zlo > 0.0 ? zlo : 0.0;
@@ -312,41 +305,45 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         lo = otf_layer_down(v, zlo);
         w = otf_layer_up(v, zhi) - lo + 1;
       }
-      s_lo[kk] = lo;
-      s_base[kk] = w;
+      sh_lo[kk] = lo;
+      sh_base[kk] = w;
     }
-    if (tid < kMaxG) s_max[tid] = 0u;
+    if (tid < kMaxG) sh_max[tid] = 0u;
     __syncthreads();
     if (warp == 0) {
       int carry = 0;
       for (int b0 = 0; b0 < nk; b0 += 32) {
         const int kk = b0 + lane;
-        const int w = kk < nk ? s_base[kk] : 0;
+        const int w = kk < nk ? sh_base[kk] : 0;
         int x = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int y = __shfl_up_sync(0xffffffffu, x, o);
           if (lane >= o) x += y;
         }
-        if (kk < nk) s_base[kk] = carry + x - w;
+        if (kk < nk) {
+          const int base = carry + x - w;
+          sh_base[kk] = base;
+          sh_kinfo[kk] = make_int2((int)sh_reg[kk] * d.NL, base - sh_lo[kk]);
+        }
         carry += __shfl_sync(0xffffffffu, x, 31);
       }
       if (lane == 0) {
-        s_base[nk] = carry;
+        sh_base[nk] = carry;
         // greedy chunks of consecutive k whose cells fit the tile
         int nc = 0, k0 = 0;
-        s_chunk[0] = 0;
+        sh_chunk[0] = 0;
         for (int kk = 0; kk < nk; ++kk) {
-          if (s_base[kk + 1] - s_base[k0] > cap_cells) {
+          if (sh_base[kk + 1] - sh_base[k0] > cap_cells) {
             if (kk == k0) {
               atomicAdd(a.err, 1);  // a single 2D segment's window exceeds the tile
               break;
             }
-            s_chunk[++nc] = kk;
+            sh_chunk[++nc] = kk;
             k0 = kk;
           }
         }
-        s_chunk[++nc] = nk;
+        sh_chunk[++nc] = nk;
         s_nchunk = nc;
       }
     }
@@ -367,26 +364,21 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
       float m = fmaxf(ph.psi[g], pb[g]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0) atomicMax(&s_max[g], __float_as_uint(m));
+      if (lane == 0) atomicMax(&sh_max[g], __float_as_uint(m));
     }
     __syncthreads();
     if (tid < G) {
-      const float b = fmaxf(__uint_as_float(s_max[tid]), a.qmax_t[(size_t)t * GP + tid]) * 1.0001f;
-      s_scale[tid] = b > 0.f ? kFixOne / b : 0.f;
-      s_iscale[tid] = b > 0.f ? b / kFixOne : 0.f;
+      const float b = fmaxf(__uint_as_float(sh_max[tid]), a.qmax_t[(size_t)t * GP + tid]) * 1.0001f;
+      sh_scale[tid] = b > 0.f ? kFixOne / b : 0.f;
+      sh_iscale[tid] = b > 0.f ? b / kFixOne : 0.f;
     }
     __syncthreads();
     const int nchunk = s_nchunk;
 #pragma unroll
-    for (int g = 0; g < G; ++g) ph.scl[g] = s_scale[g];
-    ph.s_sig = s_sig;
+    for (int g = 0; g < G; ++g) ph.scl[g] = sh_scale[g];
     ph.mat = a.mat;
     ph.qt = a.qt;
-    ph.s_reg = s_reg;
-    ph.s_base = s_base;
-    ph.s_lo = s_lo;
     ph.tile = tile;
-    ph.NL = d.NL;
     const double tn = d.an_tan[an], isn = d.an_invsin[an], Lt = d.t_len[t];
     const double z0 = z0b + (double)(U.i0 + p) * dz;
     const bool up = cot > 0;
@@ -439,17 +431,17 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
 #pragma unroll 1
       for (int ci = 0; ci < nchunk; ++ci) {
         const int c = dir == 0 ? ci : nchunk - 1 - ci;
-        const int k_lo = s_chunk[c], k_hi = s_chunk[c + 1];
-        const int cb = s_base[k_lo];
+        const int k_lo = sh_chunk[c], k_hi = sh_chunk[c + 1];
+        const int cb = sh_base[k_lo];
         ph.cbase = cb;
-        if (dir == 0) walk_fwd_chunk(w, ph, s_send, s_planes, z0, tn, isn, up, k_hi);
-        else walk_bwd_chunk(w, ph, s_send, s_planes, z0, tn, isn, up, k_lo);
+        if (dir == 0) walk_fwd_chunk(w, ph, z0, tn, isn, up, k_hi);
+        else walk_bwd_chunk(w, ph, z0, tn, isn, up, k_lo);
         __syncthreads();
         // 4. flush the chunk: c_{a,n} * fixed-point sums -> global tally (fp32 vector
         //    reductions), re-zeroing every consumed cell for the next chunk
         for (int kk = k_lo + warp; kk < k_hi; kk += nw) {
-          const int b = s_base[kk] - cb, wd = s_base[kk + 1] - s_base[kk], lo = s_lo[kk];
-          const int64_t jr = (int64_t)s_reg[kk] * d.NL + lo;
+          const int b = sh_base[kk] - cb, wd = sh_base[kk + 1] - sh_base[kk];
+          const int64_t jr = (int64_t)sh_reg[kk] * d.NL + sh_lo[kk];
           for (int x = lane; x < wd; x += 32) {
             uint32_t* cell = tile + (b + x) * stride;
             const uint32_t cnt = cell[GP];
@@ -457,7 +449,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
             float val[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) {
-              val[g] = g < G ? (float)(int)(cell[g] - cnt * kMagicBits) * (s_iscale[g] * cw) : 0.f;
+              val[g] = g < G ? (float)(int)(cell[g] - cnt * kMagicBits) * (sh_iscale[g] * cw) : 0.f;
               cell[g] = 0u;
             }
             cell[GP] = 0u;

@@ -1,0 +1,31 @@
+#!/usr/bin/env python
+"""A/B timing of the sweep kernel for a library variant (MOC3D_LIB env var selects the
+.so).  Prints one JSON line per config: median sweep ms and integrations/s.
+
+    MOC3D_LIB=paper_2503_17743_b200/libmoc3d_c2.so python tools/ab_sweep.py 4 5
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2503_17743_b200 as M  # noqa: E402
+import problems as P  # noqa: E402
+
+for cfg in [int(x) for x in sys.argv[1:]] or [4]:
+    torch.cuda.set_device(0)
+    s = M.Solver(M.Problem(P.config(cfg)))
+    s.iterate(2)
+    ms = []
+    for _ in range(5):
+        s.iterate(1)
+        ms.append(s.timings()["sweep_ms_last"])
+    t = s.timings()
+    med = float(np.median(ms))
+    print(json.dumps({"lib": os.path.basename(M.SO_PATH), "cfg": cfg, "sweep_ms": med,
+                      "integrations_per_s": t["n_integrations"] / (med * 1e-3)}), flush=True)
+    del s
