@@ -164,6 +164,12 @@ typedef struct {
   int32_t deterministic;    /* reserved (0) */
   int32_t tile_cells;       /* schedule 0: cap on FSR cells per shared-memory tally chunk
                                (0 = as many as fit; small values force many chunks, for tests) */
+  int32_t exp_mode;         /* schedule 0: 0 = pure on-the-fly (OTF); 1 = EXP/OTF hybrid of §4.2:
+                               work units sorted by segment count descending are preloaded as stored
+                               segments while the cumulative size stays within exp_fraction of the
+                               budget, the rest is traced on the fly */
+  int32_t exp_budget_mb;    /* EXP budget in MiB (0 = free device memory after allocation) */
+  double exp_fraction;      /* fraction of the budget (0 = the paper's 0.8) */
 } moc_solver_opts;
 
 /* Upload the laydown to `device`, allocate HBM state (boundary psi double buffer,
@@ -218,6 +224,8 @@ typedef struct {
   int64_t launches_per_iter; /* kernels launched per iteration */
   double setup_ms;           /* moc_solver_create wall time */
   int64_t device_bytes;      /* HBM allocated by this handle */
+  int64_t exp_segments;      /* merged 3D segments preloaded by the EXP option (0 = pure OTF) */
+  int64_t exp_bytes;         /* bytes of the EXP record store */
 } moc_timings;
 int moc_get_timings(moc_solver* s, moc_timings* t);
 

@@ -59,7 +59,8 @@ class moc_comm_desc(C.Structure):
 
 class moc_solver_opts(C.Structure):
     _fields_ = [("schedule", C.c_int32), ("threads", C.c_int32), ("blocks", C.c_int32),
-                ("deterministic", C.c_int32), ("tile_cells", C.c_int32)]
+                ("deterministic", C.c_int32), ("tile_cells", C.c_int32), ("exp_mode", C.c_int32),
+                ("exp_budget_mb", C.c_int32), ("exp_fraction", C.c_double)]
 
 
 class moc_solve_opts(C.Structure):
@@ -74,7 +75,7 @@ class moc_result(C.Structure):
 class moc_timings(C.Structure):
     _fields_ = [("n_segs3d", C.c_int64), ("n_integrations", C.c_int64), ("sweep_ms_last", C.c_double),
                 ("iter_ms_last", C.c_double), ("launches_per_iter", C.c_int64), ("setup_ms", C.c_double),
-                ("device_bytes", C.c_int64)]
+                ("device_bytes", C.c_int64), ("exp_segments", C.c_int64), ("exp_bytes", C.c_int64)]
 
 
 class moc_comm_buffers(C.Structure):
@@ -321,7 +322,8 @@ class Solver:
     """Device state + power iteration on one GPU (one rank)."""
 
     def __init__(self, problem: Problem, device: int = 0, stream=None, schedule: int = 0, threads: int = 0,
-                 blocks: int = 0, rank: int = 0, world: int = 1, tile_cells: int = 0):
+                 blocks: int = 0, rank: int = 0, world: int = 1, tile_cells: int = 0, exp_mode: int = 0,
+                 exp_budget_mb: int = 0, exp_fraction: float = 0.0):
         L = lib()
         self.problem = problem
         self._h = C.c_void_p()
@@ -331,7 +333,7 @@ class Solver:
                 stream = torch.cuda.current_stream(device).cuda_stream
             except Exception:  # torch without CUDA: legacy default stream
                 stream = 0
-        opts = moc_solver_opts(schedule, threads, blocks, 0, tile_cells)
+        opts = moc_solver_opts(schedule, threads, blocks, 0, tile_cells, exp_mode, exp_budget_mb, exp_fraction)
         comm = moc_comm_desc(rank, world, 0)
         rc = L.moc_solver_create(C.byref(self._h), problem.handle, device, C.c_void_p(stream), C.byref(comm),
                                  C.byref(opts))

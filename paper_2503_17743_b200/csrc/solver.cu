@@ -497,6 +497,13 @@ struct moc_solver {
   int* d_err = nullptr;
   int tile_words = 0;
   size_t v2_smem = 0;
+  uint32_t* d_unit_maxq = nullptr;  // longest track (merged segments) per unit
+  int scratch_q = 0;                // per-thread record capacity of the OTF scratch
+  Rec* d_scratch = nullptr;         // [sweep_blocks][scratch_q][kV2Threads]
+  // EXP preload (§4.2): record offsets per unit (kNoExp = on the fly) and the store
+  uint64_t* d_unit_exp = nullptr;
+  Rec* d_store = nullptr;
+  int64_t exp_units = 0, exp_segments = 0, exp_bytes = 0;
   // multi-GPU (world > 1)
   uint32_t *d_send_slots = nullptr, *d_recv_slots = nullptr;
   int64_t n_send = 0, n_recv = 0;
@@ -563,6 +570,11 @@ void run_sweep(moc_solver* s) {
     a.sc = s->d_sc;
     a.tile_words = s->tile_words;
     a.err = s->d_err;
+    a.unit_exp = s->d_unit_exp;
+    a.scratch = s->d_scratch;
+    a.store = s->d_store;
+    a.cost = s->d_cost;
+    a.scratch_q = s->scratch_q;
     k_sweep_v2<G, GP><<<s->sweep_blocks, kV2Threads, s->v2_smem, s->stream>>>(a);
   } else {
     k_sweep_v1<G, GP><<<s->sweep_blocks, s->sweep_threads, 0, s->stream>>>(
@@ -723,7 +735,8 @@ void destroy(moc_solver* s) {
                   s->d_an_tan, s->d_an_invsin, s->d_an_dz, s->d_an_vw, s->d_an_c, s->d_st_z0, s->d_st_first,
                   s->d_link, s->d_work, s->d_cost, s->d_mat, s->d_qt, s->d_phi, s->d_fold, s->d_fnew, s->d_tally,
                   s->d_vol, s->d_psi[0], s->d_psi[1], s->d_sc, s->d_part_a, s->d_part_b, s->d_part_c, s->d_hist,
-                  s->d_units, s->d_counter, s->d_rmax, s->d_qmax_t, s->d_tally32, s->d_err};
+                  s->d_units, s->d_counter, s->d_rmax, s->d_qmax_t, s->d_tally32, s->d_err,
+                  s->d_unit_maxq, s->d_scratch, s->d_unit_exp, s->d_store};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : s->ev)
@@ -940,12 +953,52 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       s->d_units = dmalloc<Unit>(units.size(), B);
       upload(units.data(), s->d_units, sizeof(Unit) * units.size(), st);
       uint32_t* keys = dmalloc<uint32_t>(units.size(), B);
-      k_unit_cost<<<1024, 256, 0, st>>>(s->d_units, s->n_units, s->d_st_first, s->d_cost, keys);
+      s->d_unit_maxq = dmalloc<uint32_t>(units.size(), B);
+      k_unit_cost<<<1024, 256, 0, st>>>(s->d_units, s->n_units, s->d_st_first, s->d_cost, keys, s->d_unit_maxq);
       CUDA_OK(cudaGetLastError());
       thrust::stable_sort_by_key(pol, thrust::device_ptr<uint32_t>(keys), thrust::device_ptr<uint32_t>(keys) + units.size(),
                                  thrust::device_ptr<Unit>(s->d_units), thrust::greater<uint32_t>());
+      // per-unit segment totals and longest track, in the sorted order
+      k_unit_cost<<<1024, 256, 0, st>>>(s->d_units, s->n_units, s->d_st_first, s->d_cost, keys, s->d_unit_maxq);
+      CUDA_OK(cudaGetLastError());
+      std::vector<uint32_t> ukey(units.size()), umax(units.size());
+      CUDA_OK(cudaMemcpyAsync(ukey.data(), keys, 4 * units.size(), cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaMemcpyAsync(umax.data(), s->d_unit_maxq, 4 * units.size(), cudaMemcpyDeviceToHost, st));
       CUDA_OK(cudaStreamSynchronize(st));
       cudaFree(keys);
+      s->scratch_q = 1;
+      for (uint32_t m : umax) s->scratch_q = std::max<int>(s->scratch_q, (int)m);
+      // OTF scratch: one record stream per thread of every resident CTA
+      s->d_scratch = dmalloc<Rec>((size_t)s->sweep_blocks * s->scratch_q * kV2Threads, B);
+      if (s->opts.exp_mode == 1) {
+        // §4.2: units in descending segment count, cumulated until the threshold
+        size_t freeb = 0, totalb = 0;
+        CUDA_OK(cudaMemGetInfo(&freeb, &totalb));
+        // leave room for the boundary-psi double buffer allocated below
+        const double psi_bytes = 2.0 * 2.0 * (double)s->T3 * s->GP * sizeof(float);
+        double budget = s->opts.exp_budget_mb > 0 ? s->opts.exp_budget_mb * 1048576.0 : (double)freeb - psi_bytes;
+        const double frac = s->opts.exp_fraction > 0 ? s->opts.exp_fraction : 0.8;
+        const double lim = budget * frac;
+        std::vector<uint64_t> off(units.size(), kNoExp);
+        uint64_t cum = 0;
+        for (size_t u = 0; u < units.size(); ++u) {
+          const uint64_t recs = (uint64_t)umax[u] * kV2Threads;
+          if ((double)(cum + recs) * sizeof(Rec) > lim) break;
+          off[u] = cum;
+          cum += recs;
+          s->exp_units += 1;
+          s->exp_segments += ukey[u];
+        }
+        if (s->exp_units > 0) {
+          s->exp_bytes = (int64_t)(cum * sizeof(Rec));
+          s->d_store = dmalloc<Rec>(cum, B);
+          s->d_unit_exp = dmalloc<uint64_t>(units.size(), B);
+          upload(off.data(), s->d_unit_exp, 8 * off.size(), st);
+          k_exp_generate<<<4096, kV2Threads, 0, st>>>(d, s->d_units, s->d_unit_exp, s->n_units, s->d_mat, s->d_store);
+          CUDA_OK(cudaGetLastError());
+          CUDA_OK(cudaStreamSynchronize(st));
+        }
+      }
       s->d_counter = dmalloc<uint32_t>(1, B);
       s->d_err = dmalloc<int>(1, B);
       CUDA_OK(cudaMemsetAsync(s->d_err, 0, sizeof(int), st));
@@ -1190,6 +1243,8 @@ int moc_get_timings(moc_solver* s, moc_timings* t) {
   t->launches_per_iter = 6 + (s->opts.schedule == 0 ? 2 : 0) + (s->comm.world > 1 ? 4 : 0);
   t->setup_ms = s->setup_ms;
   t->device_bytes = s->dev_bytes;
+  t->exp_segments = s->exp_segments;
+  t->exp_bytes = s->exp_bytes;
   return MOC_OK;
 }
 

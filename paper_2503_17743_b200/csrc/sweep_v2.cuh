@@ -1,5 +1,6 @@
 // sweep_v2.cuh — persistent, cost-sorted stack-band OTF sweep for sm_100a
-// (the paper's §4.3 load balancing rebuilt for Blackwell).
+// (the paper's §4.3 load balancing rebuilt for Blackwell;
+// §4.2 EXP preloading as an option).
 //
 // Work unit = (z-stack (t, n), band of <= 256 consecutive members).  One CTA of 256
 // threads takes units from a global atomic counter (units sorted by exact segment
@@ -11,28 +12,31 @@
 //      contiguous layer range [lo_k, lo_k + w_k) (Eq. 5 is linear in i and s), so the
 //      unit's FSR cells (k, layer) are packed by an exclusive scan of w_k, and cut
 //      into chunks of consecutive k whose cells fit the shared-memory tile;
-//   3. walks, one thread per track (lanes of a warp sit different members apart), the
-//      forward direction chunk by chunk and then the backward direction chunk by
-//      chunk in reverse.  The OTF walk (otf.h rules, resumable at chunk boundaries)
-//      applies Eq. 3 per segment and group and accumulates dpsi into the chunk's tile
-//      with native u32 shared atomics (ATOMS.ADD) in 2^21-scaled fixed point:
-//      r = fma(dpsi, scale, 1.5*2^23) has bits 0x4B400000 + round(dpsi*scale); the tile
-//      sums raw bits plus a per-cell segment count, the flush subtracts
-//      count * 0x4B400000 (mod 2^32).  scale = 2^21 / bound, bound >= max |dpsi| over
-//      the unit (dpsi = (psi - q)(1 - e^-tau) and psi stays between the incoming psi and
-//      the sources under the 2D track), so every term and cell sum is exact-range;
+//   3. forward direction, chunk by chunk: each thread walks one track on the fly
+//      (otf.h rules, resumable at chunk boundaries), applies Eq. 3 per merged segment
+//      and group, accumulates dpsi into the chunk's tile, and appends the merged
+//      segment as an 8-byte record {2D segment, layer, material, length} to a per-CTA
+//      scratch stream (lane-interleaved [record][thread], L2-resident); backward
+//      direction, chunks in reverse: the thread replays its records last to first
+//      (the merged list of the reversed track is the reversed list, reading Q22b), so
+//      the geometry is generated once per track per sweep.  Units preloaded by the EXP
+//      option replay both directions from a persistent record store instead.
+//      Tally accumulation uses native u32 shared atomics (ATOMS.ADD) in 2^21-scaled
+//      fixed point: r = fma(dpsi, scale, 1.5*2^23) has bits 0x4B400000 +
+//      round(dpsi*scale); the tile sums raw bits plus a per-cell segment count and the
+//      flush subtracts count * 0x4B400000 (mod 2^32).  scale = 2^21 / bound with bound
+//      >= max |dpsi| over the unit (dpsi = (psi - q)(1 - e^-tau), psi stays between the
+//      incoming psi and the sources under the 2D track), so terms and sums are exact-range;
 //   4. after each chunk, flushes its cells: c_{a,n} * sum -> tally[j][g] with
 //      red.global.add.v4.f32, re-zeroing them for the next chunk.
 // Shared-memory float atomics compile to a CAS loop on sm_100a (measured 9.9 vs 54
 // lanes/clk/SM for u32 ATOMS, profiles/micro_r1.jsonl) — hence the fixed point.
-// Per-unit tables live in static shared arrays (compile-time addresses); the tile is
-// the dynamic shared allocation.
 #pragma once
 
 namespace {
 
 #ifndef MOC_V2_CTAS_PER_SM
-#define MOC_V2_CTAS_PER_SM 3
+#define MOC_V2_CTAS_PER_SM 4
 #endif
 constexpr int kV2Threads = 256;
 constexpr int kV2MinBlocks = MOC_V2_CTAS_PER_SM;  // CTAs per SM the register/smem budget targets
@@ -41,6 +45,7 @@ constexpr int kMaxPlanes = 256;               // axial planes staged in shared m
 constexpr uint32_t kMagicBits = 0x4B400000u;  // bits of 1.5 * 2^23
 constexpr float kMagic = 12582912.0f;         // 1.5 * 2^23
 constexpr float kFixOne = 2097152.0f;         // 2^21: max |term| in fixed point
+constexpr uint64_t kNoExp = ~0ull;            // unit not preloaded (on-the-fly)
 
 // per-unit shared tables
 __shared__ double sh_send[kMaxK];        // cumulative 2D segment ends of the unit's 2D track
@@ -59,9 +64,19 @@ struct Unit {
   uint32_t stack, i0, n, cost;
 };
 
+// merged segment record: meta = kk | layer << 10 | material << 18, plus the 3D length
+struct Rec {
+  uint32_t meta;
+  float L;
+};
+__device__ __forceinline__ uint32_t rec_meta(int kk, int l, int m) {
+  return (uint32_t)kk | ((uint32_t)l << 10) | ((uint32_t)m << 18);
+}
+
 struct V2Args {
   DevData d;
   const Unit* units;
+  const uint64_t* unit_exp;  // record-store offset (in records) per unit, kNoExp = OTF
   uint32_t n_units;
   uint32_t* counter;
   const uint32_t* link;
@@ -72,6 +87,10 @@ struct V2Args {
   float* psi_out;
   float* tally;         // fp32 [J][GP]
   double* sc;
+  Rec* scratch;         // per CTA: [scratch_q][kV2Threads] records
+  const Rec* store;     // EXP record store
+  const uint32_t* cost; // exact merged segments per track (EXP replay length)
+  int scratch_q;
   int tile_words;
   int* err;
 };
@@ -90,14 +109,22 @@ __device__ __forceinline__ float attenuation_dpsi(float psi, float q, float sig_
   return fmaf(-dd, E, dd);
 }
 
-// Resumable OTF walk state of one track in one direction (same rules as otf.h).
-struct WalkState {
-  double s, s_end;  // current position and the far end (s_out forward, s_in backward)
-  int k, l;         // raw piece cursor: local 2D segment, layer
-  int pk, pl;       // pending merged segment
-  float pL, carry;
-  bool have, lead, done;
-};
+template <int GP>
+__device__ __forceinline__ void load_q(const float* qt, int64_t j, float* q) {
+  if constexpr (GP % 4 == 0) {
+#pragma unroll
+    for (int h = 0; h < GP / 4; ++h) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(qt + j * GP) + h);
+      q[4 * h] = x.x;
+      q[4 * h + 1] = x.y;
+      q[4 * h + 2] = x.z;
+      q[4 * h + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int h = 0; h < GP; ++h) q[h] = __ldg(qt + j * GP + h);
+  }
+}
 
 template <int G, int GP>
 struct Physics {
@@ -107,38 +134,16 @@ struct Physics {
   const float* qt;
   uint32_t* tile;
   int cbase;  // first cell of the current chunk
-  // source and material of the pending merged segment, loaded when the segment became
-  // pending (one raw piece ahead of its use: hides the L1/L2 latency behind the walk)
-  float pq[GP];
-  int pm;
 
-  __device__ __forceinline__ void prefetch(int kk, int l) {
-    const int64_t j = (int64_t)(sh_kinfo[kk].x + l);
-    pm = mat[j];
-    if constexpr (GP % 4 == 0) {
-#pragma unroll
-      for (int h = 0; h < GP / 4; ++h) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(qt + j * GP) + h);
-        pq[4 * h] = x.x;
-        pq[4 * h + 1] = x.y;
-        pq[4 * h + 2] = x.z;
-        pq[4 * h + 3] = x.w;
-      }
-    } else {
-#pragma unroll
-      for (int h = 0; h < GP; ++h) pq[h] = __ldg(qt + j * GP + h);
-    }
-  }
-
-  // Eq. 3 on the pending segment (kk, l) of length Lf (its data prefetched)
-  __device__ __forceinline__ void emit(int kk, int l, float Lf) {
+  // Eq. 3 on merged segment (kk, l) of material m, length Lf, source q (pre-loaded)
+  __device__ __forceinline__ void emit(int kk, int l, int m, const float* q, float Lf) {
     uint32_t* cell = tile + (sh_kinfo[kk].y - cbase + l) * (GP + 1);
     atomicAdd(cell + GP, 1u);
     float sg[GP];
     if constexpr (GP % 4 == 0) {
 #pragma unroll
       for (int h = 0; h < GP / 4; ++h) {
-        const float4 x = reinterpret_cast<const float4*>(sh_sig + pm * GP)[h];
+        const float4 x = reinterpret_cast<const float4*>(sh_sig + m * GP)[h];
         sg[4 * h] = x.x;
         sg[4 * h + 1] = x.y;
         sg[4 * h + 2] = x.z;
@@ -146,26 +151,50 @@ struct Physics {
       }
     } else {
 #pragma unroll
-      for (int h = 0; h < GP; ++h) sg[h] = sh_sig[pm * GP + h];
+      for (int h = 0; h < GP; ++h) sg[h] = sh_sig[m * GP + h];
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const float dl = attenuation_dpsi(psi[g], pq[g], sg[g], Lf);  // Eq. 3
+      const float dl = attenuation_dpsi(psi[g], q[g], sg[g], Lf);  // Eq. 3
       psi[g] -= dl;
       atomicAdd(cell + g, __float_as_uint(fmaf(dl, scl[g], kMagic)));
     }
   }
 };
 
-// forward: advance until the pending segment belongs to a chunk >= k_hi (or the end)
-template <class Ph>
-__device__ __forceinline__ void walk_fwd_chunk(WalkState& w, Ph& ph, double z0, double tn, double isn, bool up,
-                                               int k_hi) {
+// On-the-fly forward walk state (same rules as otf.h) with the pending merged
+// segment's material and source pre-loaded one raw piece ahead of its use.
+template <int GP>
+struct WalkState {
+  double s, s_end;  // current position and exit
+  int k, l;         // raw piece cursor: local 2D segment, layer
+  int pk, pl, pm;   // pending merged segment
+  float pL;
+  bool have, lead, done;
+  int nrec;         // records written
+  float pq[GP];
+
+  __device__ __forceinline__ void set_pending(int kk, int ll, const uint8_t* mat, const float* qt) {
+    pk = kk;
+    pl = ll;
+    const int64_t j = (int64_t)(sh_kinfo[kk].x + ll);
+    pm = mat[j];
+    load_q<GP>(qt, j, pq);
+  }
+};
+
+// forward OTF: advance until the pending segment belongs to a chunk >= k_hi (or the end);
+// every emitted merged segment is also appended to the thread's record stream
+template <int G, int GP>
+__device__ __forceinline__ void walk_fwd_chunk(WalkState<GP>& w, Physics<G, GP>& ph, Rec* rs, double z0, double tn,
+                                               double isn, bool up, int k_hi) {
   while (true) {
     if (w.have && w.pk >= k_hi) return;
     if (w.done) {
       if (w.have) {
-        ph.emit(w.pk, w.pl, w.pL);
+        ph.emit(w.pk, w.pl, w.pm, w.pq, w.pL);
+        rs[(size_t)w.nrec * kV2Threads] = Rec{rec_meta(w.pk, w.pl, w.pm), w.pL};
+        ++w.nrec;
         w.have = false;
       }
       return;
@@ -180,21 +209,21 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState& w, Ph& ph, double z0, 
       if (w.have) {
         w.pL += L3;
       } else {
-        w.pk = w.k;
-        w.pl = w.l;
         w.pL = L3;
         w.lead = true;
         w.have = true;
-        ph.prefetch(w.pk, w.pl);
+        w.set_pending(w.k, w.l, ph.mat, ph.qt);
       }
     } else {
-      if (w.have && !w.lead) ph.emit(w.pk, w.pl, w.pL);
+      if (w.have && !w.lead) {
+        ph.emit(w.pk, w.pl, w.pm, w.pq, w.pL);
+        rs[(size_t)w.nrec * kV2Threads] = Rec{rec_meta(w.pk, w.pl, w.pm), w.pL};
+        ++w.nrec;
+      }
       w.pL = (w.have && w.lead) ? w.pL + L3 : L3;  // a leading sliver run merges forward
-      w.pk = w.k;
-      w.pl = w.l;
       w.lead = false;
       w.have = true;
-      ph.prefetch(w.pk, w.pl);
+      w.set_pending(w.k, w.l, ph.mat, ph.qt);
     }
     if (s_next >= w.s_end) {
       w.done = true;
@@ -205,52 +234,41 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState& w, Ph& ph, double z0, 
   }
 }
 
-// backward: retreat until the pending segment belongs to a chunk < k_lo (or the start)
-template <class Ph>
-__device__ __forceinline__ void walk_bwd_chunk(WalkState& w, Ph& ph, double z0, double tn, double isn, bool up,
-                                               int k_lo) {
-  while (true) {
-    if (w.have && w.pk < k_lo) return;
-    if (w.done) {
-      if (w.have) {
-        ph.emit(w.pk, w.pl, w.pL + w.carry);
-        w.have = false;
-        w.pk = -1;
-      } else if (w.pk >= 0) {
-        if (w.pk < k_lo) return;  // all-sliver track: emit in the chunk of its last raw piece
-        ph.prefetch(w.pk, w.pl);
-        ph.emit(w.pk, w.pl, w.carry);
-        w.pk = -1;
-      }
-      return;
+// Replay of a record stream (stride kV2Threads between a thread's consecutive records),
+// records [q0, q1) in direction dq = +1 (forward) or -1 (backward), one record of
+// look-ahead (record and source loaded before the current one is applied).
+template <int GP>
+struct Replay {
+  const Rec* rs;
+  int q, qend, dq;  // next record to apply; stop index (exclusive)
+  Rec cur;
+  float cq[GP];
+  bool valid;
+
+  __device__ __forceinline__ void fetch(const float* qt) {
+    valid = q != qend;
+    if (valid) {
+      cur = rs[(size_t)q * kV2Threads];
+      const int kk = cur.meta & 1023, l = (cur.meta >> 10) & 255;
+      load_q<GP>(qt, (int64_t)(sh_kinfo[kk].x + l), cq);
     }
-    const double s_rad = w.k > 0 ? sh_send[w.k - 1] : 0.0;
-    const double s_ax = (sh_planes[up ? w.l : w.l + 1] - z0) * tn;
-    double s_prev = s_rad > s_ax ? s_rad : s_ax;
-    s_prev = s_prev > w.s_end ? s_prev : w.s_end;
-    const double L3d = (w.s - s_prev) * isn;
-    const float L3 = (float)L3d;
-    if (L3d < kEpsL) {
-      w.carry += L3;
-      if (!w.have) {
-        w.pk = w.k;  // remembered for the all-sliver case only
-        w.pl = w.l;
-      }
-    } else {
-      if (w.have) ph.emit(w.pk, w.pl, w.pL);
-      w.pk = w.k;
-      w.pl = w.l;
-      w.pL = L3 + w.carry;
-      w.carry = 0.f;
-      w.have = true;
-      ph.prefetch(w.pk, w.pl);
-    }
-    if (s_prev <= w.s_end) {
-      w.done = true;
-    } else {
-      if (s_rad >= s_ax) --w.k; else w.l -= up ? 1 : -1;
-      w.s = s_prev;
-    }
+  }
+};
+
+// apply records while they belong to the chunk [k_lo, k_hi)
+template <int G, int GP>
+__device__ __forceinline__ void replay_chunk(Replay<GP>& r, Physics<G, GP>& ph, int k_lo, int k_hi) {
+  while (r.valid) {
+    const int kk = r.cur.meta & 1023;
+    if (kk < k_lo || kk >= k_hi) return;
+    const int l = (r.cur.meta >> 10) & 255, m = r.cur.meta >> 18;
+    const float L = r.cur.L;
+    float q[GP];
+#pragma unroll
+    for (int h = 0; h < GP; ++h) q[h] = r.cq[h];
+    r.q += r.dq;
+    r.fetch(ph.qt);  // look-ahead load overlaps the physics below
+    ph.emit(kk, l, m, q, L);
   }
 }
 
@@ -272,6 +290,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
   const float ps = (float)a.sc[SC_PSI_SCALE];
   constexpr int stride = GP + 1;
   const int cap_cells = a.tile_words / stride;
+  Rec* scratch = a.scratch + (size_t)blockIdx.x * a.scratch_q * kV2Threads + tid;
   double leak = 0.0;
 
   while (true) {
@@ -281,6 +300,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const uint32_t u = s_unit;
     if (u >= a.n_units) break;
     const Unit U = a.units[u];
+    const uint64_t exp_off = a.unit_exp ? a.unit_exp[u] : kNoExp;
     const int s = (int)U.stack;
     const int t = s / d.N, n = s - t * d.N;
     const int an = d.t_a[t] * d.N + n;
@@ -382,51 +402,58 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const double tn = d.an_tan[an], isn = d.an_invsin[an], Lt = d.t_len[t];
     const double z0 = z0b + (double)(U.i0 + p) * dz;
     const bool up = cot > 0;
-    TrackGeo tg;
-    tg.z0 = z0;
-    tg.cot = cot;
-    tg.tan = tn;
-    tg.invsin = isn;
-    tg.L = Lt;
-    tg.Z = d.Z;
-    tg.sb = 0;
-    tg.se = nk;
-    double s_in = 0, s_out = 0;
-    otf_clip(tg, s_in, s_out);
     const float cw = d.an_c[an];
-#pragma unroll 1
-    for (int dir = 0; dir < 2; ++dir) {
-      WalkState w;
+    const bool otf = exp_off == kNoExp;
+    // record stream of this thread: the CTA scratch (OTF) or the unit's preloaded records
+    const Rec* rs_read = otf ? scratch : a.store + exp_off + tid;
+    int nrec = otf ? 0 : (active ? (int)a.cost[id] : 0);
+    WalkState<GP> w;
+    if (otf) {
+      TrackGeo tg;
+      tg.z0 = z0;
+      tg.cot = cot;
+      tg.tan = tn;
+      tg.invsin = isn;
+      tg.L = Lt;
+      tg.Z = d.Z;
+      tg.sb = 0;
+      tg.se = nk;
+      double s_in = 0, s_out = 0;
+      otf_clip(tg, s_in, s_out);
       w.have = false;
       w.lead = false;
       w.done = !active;
-      w.carry = 0.f;
+      w.nrec = 0;
       w.pk = -1;
       w.pl = 0;
       w.pL = 0.f;
-      if (dir == 0) {
-        w.s = s_in;
-        w.s_end = s_out;
-        if (s_in > 0.0) {
-          w.l = up ? 0 : d.NL - 1;
-          w.k = (int)otf_seg_after(v, 0, nk, s_in);
-        } else {
-          w.l = up ? otf_layer_up(v, z0) : otf_layer_down(v, z0);
-          w.k = 0;
-        }
+      w.s = s_in;
+      w.s_end = s_out;
+      if (s_in > 0.0) {
+        w.l = up ? 0 : d.NL - 1;
+        w.k = (int)otf_seg_after(v, 0, nk, s_in);
       } else {
+        w.l = up ? otf_layer_up(v, z0) : otf_layer_down(v, z0);
+        w.k = 0;
+      }
+    }
+#pragma unroll 1
+    for (int dir = 0; dir < 2; ++dir) {
+      Replay<GP> r;
+      r.rs = rs_read;
+      if (dir == 1) {
 #pragma unroll
         for (int g = 0; g < G; ++g) ph.psi[g] = pb[g];
-        w.s = s_out;
-        w.s_end = s_in;
-        if (s_out < Lt) {
-          w.l = up ? d.NL - 1 : 0;
-          w.k = (int)otf_seg_upto(v, 0, nk, s_out);
-        } else {
-          const double z_out = z0 + Lt * cot;
-          w.l = up ? otf_layer_down(v, z_out) : otf_layer_up(v, z_out);
-          w.k = nk - 1;
-        }
+        if (otf) nrec = w.nrec;
+        r.q = nrec - 1;
+        r.qend = -1;
+        r.dq = -1;
+        r.fetch(a.qt);
+      } else if (!otf) {
+        r.q = 0;
+        r.qend = nrec;
+        r.dq = 1;
+        r.fetch(a.qt);
       }
 #pragma unroll 1
       for (int ci = 0; ci < nchunk; ++ci) {
@@ -434,8 +461,8 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const int k_lo = sh_chunk[c], k_hi = sh_chunk[c + 1];
         const int cb = sh_base[k_lo];
         ph.cbase = cb;
-        if (dir == 0) walk_fwd_chunk(w, ph, z0, tn, isn, up, k_hi);
-        else walk_bwd_chunk(w, ph, z0, tn, isn, up, k_lo);
+        if (dir == 0 && otf) walk_fwd_chunk(w, ph, scratch, z0, tn, isn, up, k_hi);
+        else replay_chunk(r, ph, k_lo, k_hi);
         __syncthreads();
         // 4. flush the chunk: c_{a,n} * fixed-point sums -> global tally (fp32 vector
         //    reductions), re-zeroing every consumed cell for the next chunk
@@ -485,6 +512,32 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
   if (lane == 0 && leak != 0.0) atomicAdd(&a.sc[SC_LEAK], leak);
 }
 
+// EXP preload ("the device function for generating characteristic lines is
+// executed, and these data are stored on the GPU"): walk every track of a preloaded
+// unit once and store its merged segments as records, lane-interleaved per unit.
+__global__ void k_exp_generate(DevData d, const Unit* units, const uint64_t* unit_exp, uint32_t n_units,
+                               const uint8_t* mat, Rec* store) {
+  const OtfView v = dev_view(d);
+  for (uint32_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+    if (unit_exp[u] == kNoExp) continue;
+    const Unit U = units[u];
+    const int nact = ((int)U.n + 31) >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int p = lane * nact + warp;
+    if (warp >= nact || p >= (int)U.n) continue;
+    int s, an;
+    const uint32_t id = d.st_first[U.stack] + U.i0 + (uint32_t)p;
+    TrackGeo g = dev_track(d, id, s, an);
+    Rec* rs = store + unit_exp[u] + threadIdx.x;
+    int q = 0;
+    otf_walk_fwd(v, g, [&](int64_t k, int l, double len) {
+      const int64_t j = (int64_t)v.seg_region[k] * v.NL + l;
+      rs[(size_t)q * kV2Threads] = Rec{rec_meta((int)(k - g.sb), l, mat[j]), (float)len};
+      ++q;
+    });
+  }
+}
+
 // max qtilde over the layers of each radial region, then over the regions under each
 // 2D track: the per-unit fixed-point bound's source part (see k_sweep_v2 step 3).
 template <int G, int GP>
@@ -522,13 +575,17 @@ __global__ void k_attenuation_probe(int64_t n, const float* psi, const float* q,
 }
 
 __global__ void k_unit_cost(const Unit* units, uint32_t n_units, const uint32_t* st_first, const uint32_t* cost,
-                            uint32_t* key) {
+                            uint32_t* key, uint32_t* maxq) {
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n_units; u += gridDim.x * blockDim.x) {
     const Unit U = units[u];
     const uint32_t f = st_first[U.stack] + U.i0;
-    uint32_t c = 0;
-    for (uint32_t i = 0; i < U.n; ++i) c += cost[f + i];
+    uint32_t c = 0, mx = 0;
+    for (uint32_t i = 0; i < U.n; ++i) {
+      c += cost[f + i];
+      mx = max(mx, cost[f + i]);
+    }
     key[u] = c;
+    maxq[u] = mx;
   }
 }
 

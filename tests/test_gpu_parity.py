@@ -75,6 +75,30 @@ def test_many_chunk_tiles_parity(M, oracle_mod, tile_cells):
     assert linf < 1e-4, (linf, rel)
 
 
+@pytest.mark.parametrize("budget_mb", [0, 1])
+def test_exp_preload_parity(M, oracle_mod, budget_mb):
+    """§4.2 EXP option: preloaded units replay stored segments in both
+    directions (budget 0 = everything that fits 80% of free memory, 1 MiB = hybrid).
+    Same physics as OTF (S:348 mode equivalence): k and phi match the oracle and OTF."""
+    prob = P.with_quadrature(P.config(3), num_azim=8, num_polar=4, radial_spacing=0.5, axial_spacing=3.0)
+    pr = M.Problem(prob)
+    s = M.Solver(pr, exp_mode=1, exp_budget_mb=budget_mb)
+    t = s.timings()
+    assert t["exp_segments"] > 0
+    if budget_mb:
+        assert t["exp_segments"] < t["n_segs3d"]
+    else:
+        assert t["exp_segments"] == t["n_segs3d"]
+    k, _ = s.iterate(3)
+    ref = oracle_mod.Oracle(prob).solve(fixed_iters=3)
+    assert k == pytest.approx(ref["k"], abs=1e-5)
+    linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
+    assert linf < 1e-4, (linf, rel)
+    s0 = M.Solver(pr)
+    k0, _ = s0.iterate(3)
+    assert k == pytest.approx(k0, abs=1e-6)
+
+
 def test_cfg2_converged_parity(M, oracle_mod):
     prob = P.config(2)
     s = M.Solver(M.Problem(prob))

@@ -2,7 +2,7 @@
 """A/B timing of the sweep kernel for a library variant (MOC3D_LIB env var selects the
 .so).  Prints one JSON line per config: median sweep ms and integrations/s.
 
-    MOC3D_LIB=paper_2503_17743_b200/libmoc3d_c2.so python tools/ab_sweep.py 4 5
+    MOC3D_LIB=paper_2503_17743_b200/libmoc3d_c2.so python tools/ab_sweep.py 4 5 [--exp]
 """
 import json
 import os
@@ -16,9 +16,10 @@ import torch  # noqa: E402
 import paper_2503_17743_b200 as M  # noqa: E402
 import problems as P  # noqa: E402
 
-for cfg in [int(x) for x in sys.argv[1:]] or [4]:
+exp = "--exp" in sys.argv
+for cfg in [int(x) for x in sys.argv[1:] if not x.startswith("-")] or [4]:
     torch.cuda.set_device(0)
-    s = M.Solver(M.Problem(P.config(cfg)))
+    s = M.Solver(M.Problem(P.config(cfg)), exp_mode=1 if exp else 0)
     s.iterate(2)
     ms = []
     for _ in range(5):
@@ -26,6 +27,8 @@ for cfg in [int(x) for x in sys.argv[1:]] or [4]:
         ms.append(s.timings()["sweep_ms_last"])
     t = s.timings()
     med = float(np.median(ms))
-    print(json.dumps({"lib": os.path.basename(M.SO_PATH), "cfg": cfg, "sweep_ms": med,
-                      "integrations_per_s": t["n_integrations"] / (med * 1e-3)}), flush=True)
+    print(json.dumps({"lib": os.path.basename(M.SO_PATH), "cfg": cfg, "exp": exp, "sweep_ms": med,
+                      "integrations_per_s": t["n_integrations"] / (med * 1e-3),
+                      "exp_fraction": t["exp_segments"] / max(1, t["n_segs3d"]),
+                      "exp_gb": t["exp_bytes"] / 1e9, "setup_ms": t["setup_ms"]}), flush=True)
     del s
