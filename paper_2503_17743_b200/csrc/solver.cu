@@ -498,8 +498,6 @@ struct moc_solver {
   int tile_words = 0;
   size_t v2_smem = 0;
   uint32_t* d_unit_maxq = nullptr;  // longest track (merged segments) per unit
-  int scratch_q = 0;                // per-thread record capacity of the OTF scratch
-  Rec* d_scratch = nullptr;         // [sweep_blocks][scratch_q][kV2Threads]
   // EXP preload (§4.2): record offsets per unit (kNoExp = on the fly) and the store
   uint64_t* d_unit_exp = nullptr;
   Rec* d_store = nullptr;
@@ -571,11 +569,12 @@ void run_sweep(moc_solver* s) {
     a.tile_words = s->tile_words;
     a.err = s->d_err;
     a.unit_exp = s->d_unit_exp;
-    a.scratch = s->d_scratch;
     a.store = s->d_store;
     a.cost = s->d_cost;
-    a.scratch_q = s->scratch_q;
-    k_sweep_v2<G, GP><<<s->sweep_blocks, kV2Threads, s->v2_smem, s->stream>>>(a);
+    if (s->d_unit_exp)
+      k_sweep_v2<G, GP, true><<<s->sweep_blocks, kV2Threads, s->v2_smem, s->stream>>>(a);
+    else
+      k_sweep_v2<G, GP, false><<<s->sweep_blocks, kV2Threads, s->v2_smem, s->stream>>>(a);
   } else {
     k_sweep_v1<G, GP><<<s->sweep_blocks, s->sweep_threads, 0, s->stream>>>(
         s->dd, s->d_work, s->nwork, s->d_link, s->d_mat, s->d_qt, s->d_psi[in], s->d_psi[out], s->d_tally, s->d_sc);
@@ -586,14 +585,20 @@ template <int G, int GP>
 void v2_configure(moc_solver* s) {
   // kV2MinBlocks CTAs per SM: 228 KB of shared memory per SM, 1 KB reserved per CTA;
   // the dynamic part (the tally tile) is what the static per-unit tables leave.
-  cudaFuncAttributes fa{};
-  CUDA_OK(cudaFuncGetAttributes(&fa, k_sweep_v2<G, GP>));
+  cudaFuncAttributes fa{}, fb{};
+  CUDA_OK(cudaFuncGetAttributes(&fa, k_sweep_v2<G, GP, false>));
+  CUDA_OK(cudaFuncGetAttributes(&fb, k_sweep_v2<G, GP, true>));
   const size_t per_cta = (228 * 1024) / kV2MinBlocks - 1024;
-  s->v2_smem = (per_cta - fa.sharedSizeBytes) & ~size_t(15);
+  s->v2_smem = (per_cta - std::max(fa.sharedSizeBytes, fb.sharedSizeBytes)) & ~size_t(15);
   s->tile_words = (int)(s->v2_smem / 4);
-  CUDA_OK(cudaFuncSetAttribute(k_sweep_v2<G, GP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->v2_smem));
-  int per_sm = 0;
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_v2<G, GP>, kV2Threads, s->v2_smem));
+  CUDA_OK(cudaFuncSetAttribute(k_sweep_v2<G, GP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)s->v2_smem));
+  CUDA_OK(cudaFuncSetAttribute(k_sweep_v2<G, GP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)s->v2_smem));
+  int per_sm = 0, per_sm_b = 0;
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_v2<G, GP, false>, kV2Threads, s->v2_smem));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_b, k_sweep_v2<G, GP, true>, kV2Threads, s->v2_smem));
+  per_sm = std::min(per_sm, per_sm_b);
   if (per_sm < 1) throw Error(MOC_E_CAPACITY, "sweep kernel does not fit on an SM");
   int dev = 0, nsm = 0;
   CUDA_OK(cudaGetDevice(&dev));
@@ -736,7 +741,7 @@ void destroy(moc_solver* s) {
                   s->d_link, s->d_work, s->d_cost, s->d_mat, s->d_qt, s->d_phi, s->d_fold, s->d_fnew, s->d_tally,
                   s->d_vol, s->d_psi[0], s->d_psi[1], s->d_sc, s->d_part_a, s->d_part_b, s->d_part_c, s->d_hist,
                   s->d_units, s->d_counter, s->d_rmax, s->d_qmax_t, s->d_tally32, s->d_err,
-                  s->d_unit_maxq, s->d_scratch, s->d_unit_exp, s->d_store};
+                  s->d_unit_maxq, s->d_unit_exp, s->d_store};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : s->ev)
@@ -966,10 +971,6 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       CUDA_OK(cudaMemcpyAsync(umax.data(), s->d_unit_maxq, 4 * units.size(), cudaMemcpyDeviceToHost, st));
       CUDA_OK(cudaStreamSynchronize(st));
       cudaFree(keys);
-      s->scratch_q = 1;
-      for (uint32_t m : umax) s->scratch_q = std::max<int>(s->scratch_q, (int)m);
-      // OTF scratch: one record stream per thread of every resident CTA
-      s->d_scratch = dmalloc<Rec>((size_t)s->sweep_blocks * s->scratch_q * kV2Threads, B);
       if (s->opts.exp_mode == 1) {
         // §4.2: units in descending segment count, cumulated until the threshold
         size_t freeb = 0, totalb = 0;

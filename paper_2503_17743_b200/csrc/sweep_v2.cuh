@@ -12,15 +12,12 @@
 //      contiguous layer range [lo_k, lo_k + w_k) (Eq. 5 is linear in i and s), so the
 //      unit's FSR cells (k, layer) are packed by an exclusive scan of w_k, and cut
 //      into chunks of consecutive k whose cells fit the shared-memory tile;
-//   3. forward direction, chunk by chunk: each thread walks one track on the fly
-//      (otf.h rules, resumable at chunk boundaries), applies Eq. 3 per merged segment
-//      and group, accumulates dpsi into the chunk's tile, and appends the merged
-//      segment as an 8-byte record {2D segment, layer, material, length} to a per-CTA
-//      scratch stream (lane-interleaved [record][thread], L2-resident); backward
-//      direction, chunks in reverse: the thread replays its records last to first
-//      (the merged list of the reversed track is the reversed list, reading Q22b), so
-//      the geometry is generated once per track per sweep.  Units preloaded by the EXP
-//      option replay both directions from a persistent record store instead.
+//   3. each thread walks one track on the fly (otf.h rules, resumable at chunk
+//      boundaries), forward chunk by chunk, then backward through the chunks in
+//      reverse, applying Eq. 3 per merged segment and group and accumulating dpsi into
+//      the chunk's tile.  Units preloaded by the EXP option replay stored 8-byte
+//      records {2D segment, layer, material, length} in both directions instead (on
+//      B200 this measured slower than regenerating the geometry: DESIGN.md §5).
 //      Tally accumulation uses native u32 shared atomics (ATOMS.ADD) in 2^21-scaled
 //      fixed point: r = fma(dpsi, scale, 1.5*2^23) has bits 0x4B400000 +
 //      round(dpsi*scale); the tile sums raw bits plus a per-cell segment count and the
@@ -87,10 +84,8 @@ struct V2Args {
   float* psi_out;
   float* tally;         // fp32 [J][GP]
   double* sc;
-  Rec* scratch;         // per CTA: [scratch_q][kV2Threads] records
   const Rec* store;     // EXP record store
   const uint32_t* cost; // exact merged segments per track (EXP replay length)
-  int scratch_q;
   int tile_words;
   int* err;
 };
@@ -166,12 +161,11 @@ struct Physics {
 // segment's material and source pre-loaded one raw piece ahead of its use.
 template <int GP>
 struct WalkState {
-  double s, s_end;  // current position and exit
+  double s, s_end;  // current position and the far end (s_out forward, s_in backward)
   int k, l;         // raw piece cursor: local 2D segment, layer
   int pk, pl, pm;   // pending merged segment
-  float pL;
+  float pL, carry;
   bool have, lead, done;
-  int nrec;         // records written
   float pq[GP];
 
   __device__ __forceinline__ void set_pending(int kk, int ll, const uint8_t* mat, const float* qt) {
@@ -183,18 +177,15 @@ struct WalkState {
   }
 };
 
-// forward OTF: advance until the pending segment belongs to a chunk >= k_hi (or the end);
-// every emitted merged segment is also appended to the thread's record stream
+// forward OTF: advance until the pending segment belongs to a chunk >= k_hi (or the end)
 template <int G, int GP>
-__device__ __forceinline__ void walk_fwd_chunk(WalkState<GP>& w, Physics<G, GP>& ph, Rec* rs, double z0, double tn,
+__device__ __forceinline__ void walk_fwd_chunk(WalkState<GP>& w, Physics<G, GP>& ph, double z0, double tn,
                                                double isn, bool up, int k_hi) {
   while (true) {
     if (w.have && w.pk >= k_hi) return;
     if (w.done) {
       if (w.have) {
         ph.emit(w.pk, w.pl, w.pm, w.pq, w.pL);
-        rs[(size_t)w.nrec * kV2Threads] = Rec{rec_meta(w.pk, w.pl, w.pm), w.pL};
-        ++w.nrec;
         w.have = false;
       }
       return;
@@ -215,11 +206,7 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<GP>& w, Physics<G, GP>&
         w.set_pending(w.k, w.l, ph.mat, ph.qt);
       }
     } else {
-      if (w.have && !w.lead) {
-        ph.emit(w.pk, w.pl, w.pm, w.pq, w.pL);
-        rs[(size_t)w.nrec * kV2Threads] = Rec{rec_meta(w.pk, w.pl, w.pm), w.pL};
-        ++w.nrec;
-      }
+      if (w.have && !w.lead) ph.emit(w.pk, w.pl, w.pm, w.pq, w.pL);
       w.pL = (w.have && w.lead) ? w.pL + L3 : L3;  // a leading sliver run merges forward
       w.lead = false;
       w.have = true;
@@ -230,6 +217,55 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<GP>& w, Physics<G, GP>&
     } else {
       if (s_rad <= s_ax) ++w.k; else w.l += up ? 1 : -1;
       w.s = s_next;
+    }
+  }
+}
+
+// backward OTF: retreat until the pending segment belongs to a chunk < k_lo (or the
+// start).  Short raw pieces are carried into the next long one, so the merged list is
+// the reverse of the forward one (reading Q22b).
+template <int G, int GP>
+__device__ __forceinline__ void walk_bwd_chunk(WalkState<GP>& w, Physics<G, GP>& ph, double z0, double tn,
+                                               double isn, bool up, int k_lo) {
+  while (true) {
+    if (w.have && w.pk < k_lo) return;
+    if (w.done) {
+      if (w.have) {
+        ph.emit(w.pk, w.pl, w.pm, w.pq, w.pL + w.carry);
+        w.have = false;
+        w.pk = -1;
+      } else if (w.pk >= 0) {
+        if (w.pk < k_lo) return;  // all-sliver track: emit in the chunk of its last raw piece
+        w.set_pending(w.pk, w.pl, ph.mat, ph.qt);
+        ph.emit(w.pk, w.pl, w.pm, w.pq, w.carry);
+        w.pk = -1;
+      }
+      return;
+    }
+    const double s_rad = w.k > 0 ? sh_send[w.k - 1] : 0.0;
+    const double s_ax = (sh_planes[up ? w.l : w.l + 1] - z0) * tn;
+    double s_prev = s_rad > s_ax ? s_rad : s_ax;
+    s_prev = s_prev > w.s_end ? s_prev : w.s_end;
+    const double L3d = (w.s - s_prev) * isn;
+    const float L3 = (float)L3d;
+    if (L3d < kEpsL) {
+      w.carry += L3;
+      if (!w.have) {
+        w.pk = w.k;  // remembered for the all-sliver case only
+        w.pl = w.l;
+      }
+    } else {
+      if (w.have) ph.emit(w.pk, w.pl, w.pm, w.pq, w.pL);
+      w.pL = L3 + w.carry;
+      w.carry = 0.f;
+      w.have = true;
+      w.set_pending(w.k, w.l, ph.mat, ph.qt);
+    }
+    if (s_prev <= w.s_end) {
+      w.done = true;
+    } else {
+      if (s_rad >= s_ax) --w.k; else w.l -= up ? 1 : -1;
+      w.s = s_prev;
     }
   }
 }
@@ -272,7 +308,9 @@ __device__ __forceinline__ void replay_chunk(Replay<GP>& r, Physics<G, GP>& ph, 
   }
 }
 
-template <int G, int GP>
+// HYBRID = false: pure on-the-fly sweep (the replay path is not compiled in, which keeps
+// the register budget for the walk); true: units may be EXP-preloaded.
+template <int G, int GP, bool HYBRID>
 __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a) {
   extern __shared__ __align__(16) uint32_t tile[];
   __shared__ uint32_t s_unit;
@@ -290,7 +328,6 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
   const float ps = (float)a.sc[SC_PSI_SCALE];
   constexpr int stride = GP + 1;
   const int cap_cells = a.tile_words / stride;
-  Rec* scratch = a.scratch + (size_t)blockIdx.x * a.scratch_q * kV2Threads + tid;
   double leak = 0.0;
 
   while (true) {
@@ -300,7 +337,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const uint32_t u = s_unit;
     if (u >= a.n_units) break;
     const Unit U = a.units[u];
-    const uint64_t exp_off = a.unit_exp ? a.unit_exp[u] : kNoExp;
+    const uint64_t exp_off = HYBRID ? a.unit_exp[u] : kNoExp;
     const int s = (int)U.stack;
     const int t = s / d.N, n = s - t * d.N;
     const int an = d.t_a[t] * d.N + n;
@@ -403,11 +440,8 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const double z0 = z0b + (double)(U.i0 + p) * dz;
     const bool up = cot > 0;
     const float cw = d.an_c[an];
-    const bool otf = exp_off == kNoExp;
-    // record stream of this thread: the CTA scratch (OTF) or the unit's preloaded records
-    const Rec* rs_read = otf ? scratch : a.store + exp_off + tid;
-    int nrec = otf ? 0 : (active ? (int)a.cost[id] : 0);
-    WalkState<GP> w;
+    const bool otf = !HYBRID || exp_off == kNoExp;
+    double s_in = 0, s_out = 0;
     if (otf) {
       TrackGeo tg;
       tg.z0 = z0;
@@ -418,41 +452,53 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
       tg.Z = d.Z;
       tg.sb = 0;
       tg.se = nk;
-      double s_in = 0, s_out = 0;
       otf_clip(tg, s_in, s_out);
-      w.have = false;
-      w.lead = false;
-      w.done = !active;
-      w.nrec = 0;
-      w.pk = -1;
-      w.pl = 0;
-      w.pL = 0.f;
-      w.s = s_in;
-      w.s_end = s_out;
-      if (s_in > 0.0) {
-        w.l = up ? 0 : d.NL - 1;
-        w.k = (int)otf_seg_after(v, 0, nk, s_in);
-      } else {
-        w.l = up ? otf_layer_up(v, z0) : otf_layer_down(v, z0);
-        w.k = 0;
-      }
     }
 #pragma unroll 1
     for (int dir = 0; dir < 2; ++dir) {
-      Replay<GP> r;
-      r.rs = rs_read;
       if (dir == 1) {
 #pragma unroll
         for (int g = 0; g < G; ++g) ph.psi[g] = pb[g];
-        if (otf) nrec = w.nrec;
-        r.q = nrec - 1;
-        r.qend = -1;
-        r.dq = -1;
-        r.fetch(a.qt);
-      } else if (!otf) {
-        r.q = 0;
-        r.qend = nrec;
-        r.dq = 1;
+      }
+      WalkState<GP> w;
+      Replay<GP> r;
+      if (otf) {
+        w.have = false;
+        w.lead = false;
+        w.done = !active;
+        w.carry = 0.f;
+        w.pk = -1;
+        w.pl = 0;
+        w.pL = 0.f;
+        if (dir == 0) {
+          w.s = s_in;
+          w.s_end = s_out;
+          if (s_in > 0.0) {
+            w.l = up ? 0 : d.NL - 1;
+            w.k = (int)otf_seg_after(v, 0, nk, s_in);
+          } else {
+            w.l = up ? otf_layer_up(v, z0) : otf_layer_down(v, z0);
+            w.k = 0;
+          }
+        } else {
+          w.s = s_out;
+          w.s_end = s_in;
+          if (s_out < Lt) {
+            w.l = up ? d.NL - 1 : 0;
+            w.k = (int)otf_seg_upto(v, 0, nk, s_out);
+          } else {
+            const double z_out = z0 + Lt * cot;
+            w.l = up ? otf_layer_down(v, z_out) : otf_layer_up(v, z_out);
+            w.k = nk - 1;
+          }
+        }
+      } else {
+        // EXP: this thread's preloaded records, first to last or last to first
+        const int nrec = active ? (int)a.cost[id] : 0;
+        r.rs = a.store + exp_off + tid;
+        r.q = dir == 0 ? 0 : nrec - 1;
+        r.qend = dir == 0 ? nrec : -1;
+        r.dq = dir == 0 ? 1 : -1;
         r.fetch(a.qt);
       }
 #pragma unroll 1
@@ -461,8 +507,9 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const int k_lo = sh_chunk[c], k_hi = sh_chunk[c + 1];
         const int cb = sh_base[k_lo];
         ph.cbase = cb;
-        if (dir == 0 && otf) walk_fwd_chunk(w, ph, scratch, z0, tn, isn, up, k_hi);
-        else replay_chunk(r, ph, k_lo, k_hi);
+        if (!otf) replay_chunk(r, ph, k_lo, k_hi);
+        else if (dir == 0) walk_fwd_chunk(w, ph, z0, tn, isn, up, k_hi);
+        else walk_bwd_chunk(w, ph, z0, tn, isn, up, k_lo);
         __syncthreads();
         // 4. flush the chunk: c_{a,n} * fixed-point sums -> global tally (fp32 vector
         //    reductions), re-zeroing every consumed cell for the next chunk
