@@ -125,6 +125,25 @@ def oracle_sample(prob, target_s: float = 15.0):
                 seconds=sec, integrations=nint)
 
 
+def k_eff_errors(M, dev):
+    """BASELINE metric's 'k-eff err' on problems with a closed-form answer (the oracle
+    parity at full size lives in tests/test_gpu_parity.py): converged k of the 1-group
+    reflective cube vs nuSf/Sa = 1.5 and of the 7-group cube vs the dominant
+    eigenvalue of the dense G x G matrix."""
+    out = {}
+    for variant in ("1g", "7g"):
+        prob = P.config1(variant)
+        s = M.Solver(M.Problem(prob), device=dev)
+        r = s.solve(tol_k=1e-10, tol_src=1e-8, max_iter=20000, check_every=20)
+        m = prob["materials"][0]
+        A = np.diag(m["sigma_t"]) - np.array(m["sigma_s"]).T
+        kd = float(max(abs(np.linalg.eigvals(np.linalg.solve(A, np.outer(m["chi"], m["nu_sigma_f"]))))))
+        out[f"cfg1_{variant}"] = {"k_gpu": r["k"], "k_exact": kd, "abs_err": abs(r["k"] - kd),
+                                  "iterations": r["iterations"]}
+        del s
+    return out
+
+
 def run_reference(args):
     rank, world, _ = _dist_env()
     if rank != 0:
@@ -169,7 +188,7 @@ def run_ours(args):
     t_lay = time.time() - t0
     st = pr.stats()
     t0 = time.time()
-    s = M.Solver(pr, device=dev, schedule=args.schedule, rank=rank, world=world)
+    s = M.Solver(pr, device=dev, schedule=args.schedule, rank=rank, world=world, exp_mode=1 if args.exp else 0)
     t_setup = time.time() - t0
     tm = s.timings()
     G = pr.G
@@ -227,6 +246,7 @@ def run_ours(args):
     sweep_med = float(np.median(sweep_ms))
     achieved = nint / (sweep_med * 1e-3)
     peak = r_alu(G, mhz_max)
+    kerr = k_eff_errors(M, dev) if rank == 0 and not args.no_parity else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = oracle_sample(prob, target_s=args.ref_seconds)
@@ -259,6 +279,8 @@ def run_ours(args):
         "gpu_launches": tm["launches_per_iter"] * args.steps,
         "clocks": clocks,
         "cpu_baseline": cpu,
+        "k_eff_err": kerr,
+        "sweep_s_per_iter": sweep_med * 1e-3,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -276,6 +298,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--schedule", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the closed-form k-eff error legs")
+    ap.add_argument("--exp", action="store_true", help="EXP/OTF hybrid of §4.2 instead of pure OTF")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     args = ap.parse_args()
     if args.impl == "reference":

@@ -148,6 +148,22 @@ def test_checksums_full_size_sampled(M, oracle_mod, cfg):
     assert s.fsr_volumes().sum() == pytest.approx(W * W * Z, rel=1e-10)
 
 
+@pytest.mark.parametrize("cfg,iters", [(3, 3), (4, 2)])
+def test_full_size_fixed_iteration_parity(M, oracle_mod, cfg, iters):
+    """BASELINE sizes in the launch configuration bench.py times (schedule 0, default
+    tiles): k and every FSR flux after `iters` power iterations from phi = 1, k = 1,
+    psi = 0 against the fp64 oracle (fixed-N parity for cfg4)."""
+    prob = P.config(cfg)
+    s = M.Solver(M.Problem(prob))
+    k, _ = s.iterate(iters)
+    ref = oracle_mod.Oracle(prob).solve(fixed_iters=iters)
+    assert k == pytest.approx(ref["k"], abs=1e-5)
+    linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
+    assert linf < 1e-4, (linf, rel)
+    kh, _ = s.history()
+    np.testing.assert_allclose(kh, ref["k_hist"], atol=1e-5)
+
+
 def test_cfg3_reduced_fixed_iterations(M, oracle_mod):
     """C5G7 assembly geometry with coarser tracking (many work units, ragged
     stacks): 3 fixed iterations against the oracle."""
