@@ -226,6 +226,9 @@ typedef struct {
   int64_t device_bytes;      /* HBM allocated by this handle */
   int64_t exp_segments;      /* merged 3D segments preloaded by the EXP option (0 = pure OTF) */
   int64_t exp_bytes;         /* bytes of the EXP record store */
+  int64_t emitted_last;      /* merged segment-direction applications of Eq. 3-4 in the last
+                                iteration's sweep on this rank (integrity counter: equals
+                                2 * n_segs3d on one GPU); -1 if it could not be read */
 } moc_timings;
 int moc_get_timings(moc_solver* s, moc_timings* t);
 

@@ -75,7 +75,8 @@ class moc_result(C.Structure):
 class moc_timings(C.Structure):
     _fields_ = [("n_segs3d", C.c_int64), ("n_integrations", C.c_int64), ("sweep_ms_last", C.c_double),
                 ("iter_ms_last", C.c_double), ("launches_per_iter", C.c_int64), ("setup_ms", C.c_double),
-                ("device_bytes", C.c_int64), ("exp_segments", C.c_int64), ("exp_bytes", C.c_int64)]
+                ("device_bytes", C.c_int64), ("exp_segments", C.c_int64), ("exp_bytes", C.c_int64),
+                ("emitted_last", C.c_int64)]
 
 
 class moc_comm_buffers(C.Structure):

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -61,6 +62,8 @@ enum {
   SC_LEAK_SCALED,
   SC_BAD,          // count of NaN/negative fluxes in the last finalize
   SC_ITER,         // completed iterations
+  SC_NEMIT,        // merged segment-direction emissions of the running sweep (this rank)
+  SC_NEMIT_LAST,   // ... of the last completed iteration
   SC_N
 };
 
@@ -218,6 +221,7 @@ __global__ void __launch_bounds__(512) k_sweep_v1(DevData d, const uint32_t* wor
   const OtfView v = dev_view(d);
   const float ps = (float)sc[SC_PSI_SCALE];
   double leak = 0;
+  uint64_t nemit = 0;
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwork; w += gridDim.x * blockDim.x) {
     const uint32_t id = work[w];
     int s, an;
@@ -229,6 +233,7 @@ __global__ void __launch_bounds__(512) k_sweep_v1(DevData d, const uint32_t* wor
 #pragma unroll
       for (int q = 0; q < G; ++q) psi[q] = psi_in[(size_t)slot * GP + q] * ps;
       auto seg = [&](int64_t k, int l, double len) {
+        ++nemit;
         const int64_t j = (int64_t)v.seg_region[k] * v.NL + l;
         const float Lf = (float)len;
         const int m = mat[j];
@@ -254,8 +259,12 @@ __global__ void __launch_bounds__(512) k_sweep_v1(DevData d, const uint32_t* wor
       }
     }
   }
-  for (int o = 16; o > 0; o >>= 1) leak += __shfl_xor_sync(0xffffffffu, leak, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    leak += __shfl_xor_sync(0xffffffffu, leak, o);
+    nemit += __shfl_xor_sync(0xffffffffu, nemit, o);
+  }
   if ((threadIdx.x & 31) == 0 && leak != 0.0) atomicAdd(&sc[SC_LEAK], leak);
+  if ((threadIdx.x & 31) == 0 && nemit) atomicAdd(&sc[SC_NEMIT], (double)nemit);
 }
 
 // ------------------------------------------------------------ A7: finalize
@@ -406,6 +415,8 @@ __global__ void k_resid(const double* part2, int nb, double* sc, double* hist, i
     }
     sc[SC_ITER] = it + 1;
     sc[SC_LEAK] = 0.0;
+    sc[SC_NEMIT_LAST] = sc[SC_NEMIT];
+    sc[SC_NEMIT] = 0.0;
   }
 }
 
@@ -496,6 +507,8 @@ struct moc_solver {
   float *d_rmax = nullptr, *d_qmax_t = nullptr, *d_tally32 = nullptr;
   int* d_err = nullptr;
   int tile_words = 0;
+  int lane_lg = -1;  // forced log2 v2 lane stride (MOC_V2_LANE_STRIDE), -1 = per unit
+  double h_lane = 0;     // thinnest axial layer / 3 (sweep_v2.cuh lane_lg_of)
   size_t v2_smem = 0;
   uint32_t* d_unit_maxq = nullptr;  // longest track (merged segments) per unit
   // EXP preload (§4.2): record offsets per unit (kNoExp = on the fly) and the store
@@ -567,6 +580,8 @@ void run_sweep(moc_solver* s) {
     a.tally = s->d_tally32;
     a.sc = s->d_sc;
     a.tile_words = s->tile_words;
+    a.lane_lg = s->lane_lg;
+    a.h_lane = s->h_lane;
     a.err = s->d_err;
     a.unit_exp = s->d_unit_exp;
     a.store = s->d_store;
@@ -947,6 +962,16 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
         if (s->opts.tile_cells < g.NL) throw Error(MOC_E_PARAM, "tile_cells must be >= the number of axial layers");
         s->tile_words = std::min(s->tile_words, s->opts.tile_cells * (s->GP + 1));
       }
+      {
+        double hmin = 1e300;
+        for (int l = 0; l < g.NL; ++l) hmin = std::min(hmin, g.planes[l + 1] - g.planes[l]);
+        const char* dv = std::getenv("MOC_V2_LANE_DIV");  // A/B override of the 1/3
+        s->h_lane = hmin / (dv ? std::atof(dv) : 3.0);
+        if (const char* e = std::getenv("MOC_V2_LANE_STRIDE")) {  // A/B override
+          const int v = std::atoi(e);
+          s->lane_lg = v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0;
+        }
+      }
       std::vector<Unit> units;
       for (int64_t q = 0; q < s->S; ++q) {
         if (!owner.empty() && owner[q] != s->comm.rank) continue;
@@ -995,7 +1020,7 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
           s->d_store = dmalloc<Rec>(cum, B);
           s->d_unit_exp = dmalloc<uint64_t>(units.size(), B);
           upload(off.data(), s->d_unit_exp, 8 * off.size(), st);
-          k_exp_generate<<<4096, kV2Threads, 0, st>>>(d, s->d_units, s->d_unit_exp, s->n_units, s->d_mat, s->d_store);
+          k_exp_generate<<<4096, kV2Threads, 0, st>>>(d, s->d_units, s->d_unit_exp, s->n_units, s->d_mat, s->d_store, s->h_lane, s->lane_lg);
           CUDA_OK(cudaGetLastError());
           CUDA_OK(cudaStreamSynchronize(st));
         }
@@ -1246,6 +1271,12 @@ int moc_get_timings(moc_solver* s, moc_timings* t) {
   t->device_bytes = s->dev_bytes;
   t->exp_segments = s->exp_segments;
   t->exp_bytes = s->exp_bytes;
+  double sc[SC_N];
+  t->emitted_last = -1;
+  if (cudaMemcpyAsync(sc, s->d_sc, sizeof(sc), cudaMemcpyDeviceToHost, s->stream) == cudaSuccess &&
+      cudaStreamSynchronize(s->stream) == cudaSuccess)
+    t->emitted_last = (int64_t)sc[SC_NEMIT_LAST];
+  (void)cudaGetLastError();
   return MOC_OK;
 }
 

@@ -45,7 +45,7 @@ constexpr float kFixOne = 2097152.0f;         // 2^21: max |term| in fixed point
 constexpr uint64_t kNoExp = ~0ull;            // unit not preloaded (on-the-fly)
 
 // per-unit shared tables
-__shared__ double sh_send[kMaxK];        // cumulative 2D segment ends of the unit's 2D track
+__shared__ double sh_sendx[kMaxK + 1];   // [0] = 0, [k + 1] = cumulative end of 2D segment k
 __shared__ double sh_planes[kMaxPlanes]; // axial planes
 __shared__ int2 sh_kinfo[kMaxK];         // {region * NL, first tile cell of k - lo_k}
 __shared__ uint32_t sh_reg[kMaxK];
@@ -87,8 +87,30 @@ struct V2Args {
   const Rec* store;     // EXP record store
   const uint32_t* cost; // exact merged segments per track (EXP replay length)
   int tile_words;
+  double h_lane;            // thinnest axial layer / 3 (lane_lg_of)
+  int lane_lg;          // forced log2 lane stride, -1 = per unit (lane_lg_of)
   int* err;
 };
+
+// Stack member (within the unit's band) walked by thread tid, for a lane stride of
+// 2^lg members: groups of 2^lg warps cover 32 * 2^lg consecutive members, lane i of a
+// warp taking every 2^lg-th.  Neighbouring z-members have nearly equal 3D lengths (busy
+// SIMT lanes: lane efficiency 0.90 contiguous vs 0.76 spread over the band on cfg4,
+// tools/lane_eff.py) but cross the same FSR at the same time (same-address shared
+// atomics serialise); the stride trades the two.  lane_lg_of picks it per unit from the
+// stack's member spacing dz: the smallest 2^lg (<= 8) with 2^lg dz >= h_min / 3 (about
+// 3 lanes per layer thickness) while 2^lg warps stay busy on the band's n members
+// (A/B over the divisor and forced strides on cfg4 / cfg5: profiles/README.md).
+__device__ __forceinline__ int lane_lg_of(double dz, double h_lane, int forced, int n) {
+  if (forced >= 0) return forced;
+  int lg = 0;
+  while (lg < 3 && (double)(1 << lg) * dz < h_lane && (64 << lg) <= n + 31) ++lg;  // 2^(lg+1) warps busy
+  return lg;
+}
+__device__ __forceinline__ int member_of(int tid, int lg) {
+  const int w = tid >> 5, lane = tid & 31;
+  return ((w >> lg) << (5 + lg)) + (lane << lg) + (w & ((1 << lg) - 1));
+}
 
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float e) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(e)
@@ -121,18 +143,30 @@ __device__ __forceinline__ void load_q(const float* qt, int64_t j, float* q) {
   }
 }
 
+// Eq. 3 + Eq. 4 for one merged segment in all groups.  psi is carried in the unit's
+// fixed-point units (psi' = psi * scale_g, scale_g = 2^21 / bound_g), so the tally term
+// dpsi' = (psi' - q scale_g)(1 - e^{-tau}) is already scaled and its fixed-point code is
+// one FADD with the 1.5 * 2^23 magic: per group FMUL, MUFU.EX2, 2 FFMA, 2 FADD, ATOMS.
 template <int G, int GP>
 struct Physics {
   float psi[G];
   float scl[G];
   const uint8_t* mat;
   const float* qt;
-  uint32_t* tile;
-  int cbase;  // first cell of the current chunk
+  uint32_t* ctile;  // tile - (first cell of the current chunk) * (GP + 1)
 
-  // Eq. 3 on merged segment (kk, l) of material m, length Lf, source q (pre-loaded)
-  __device__ __forceinline__ void emit(int kk, int l, int m, const float* q, float Lf) {
-    uint32_t* cell = tile + (sh_kinfo[kk].y - cbase + l) * (GP + 1);
+#ifdef MOC_DEBUG_WALK
+  int dbg_lo, dbg_hi, dbg_dir, dbg_k, dbg_l;
+#endif
+  __device__ __forceinline__ void emit(int pc, int m, const float* q, float Lf) {
+#ifdef MOC_DEBUG_WALK
+    if (pc < dbg_lo || pc >= dbg_hi) {
+      printf("bad emit: blk %d tid %d dir %d pc %d chunk [%d,%d) k %d l %d m %d L %g\n", blockIdx.x, threadIdx.x,
+             dbg_dir, pc, dbg_lo, dbg_hi, dbg_k, dbg_l, m, Lf);
+      return;
+    }
+#endif
+    uint32_t* cell = ctile + pc * (GP + 1);
     atomicAdd(cell + GP, 1u);
     float sg[GP];
     if constexpr (GP % 4 == 0) {
@@ -150,122 +184,167 @@ struct Physics {
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const float dl = attenuation_dpsi(psi[g], q[g], sg[g], Lf);  // Eq. 3
+      const float E = ex2_approx(-sg[g] * Lf);
+      const float dd = fmaf(-q[g], scl[g], psi[g]);
+      const float dl = fmaf(-dd, E, dd);  // (psi' - q')(1 - E)
       psi[g] -= dl;
-      atomicAdd(cell + g, __float_as_uint(fmaf(dl, scl[g], kMagic)));
+      atomicAdd(cell + g, __float_as_uint(dl + kMagic));
     }
   }
 };
 
-// On-the-fly forward walk state (same rules as otf.h) with the pending merged
-// segment's material and source pre-loaded one raw piece ahead of its use.
+// On-the-fly walk state (same piece and merge rules as otf.h, reading Q22b).  The
+// next radial and axial crossings are cached (s_rad, s_ax) and refreshed only for the
+// boundary just crossed.  Pending merged segment: pc = its tile cell index (-1 = none;
+// cells of 2D segment k are [base_k, base_k+1), so chunk membership is a compare on
+// pc), pm / pq = material and source loaded when it was set (one raw piece ahead of
+// use).  carry = sliver length not yet attached to a long piece; fkl = first sliver
+// (k | l << 16) seen while nothing is pending (all-sliver tracks only, else -1).
 template <int GP>
 struct WalkState {
-  double s, s_end;  // current position and the far end (s_out forward, s_in backward)
-  int k, l;         // raw piece cursor: local 2D segment, layer
-  int pk, pl, pm;   // pending merged segment
+  double s, s_end, s_rad, s_ax;
+  int k, l, pc, pm, fkl;
   float pL, carry;
-  bool have, lead, done;
+  bool done;
   float pq[GP];
 
   __device__ __forceinline__ void set_pending(int kk, int ll, const uint8_t* mat, const float* qt) {
-    pk = kk;
-    pl = ll;
-    const int64_t j = (int64_t)(sh_kinfo[kk].x + ll);
+    const int2 ki = sh_kinfo[kk];
+    const int64_t j = (int64_t)(ki.x + ll);
+    pc = ki.y + ll;
+#ifdef MOC_DEBUG_WALK
+    if (pc < sh_base[kk] || pc >= sh_base[kk + 1])
+      printf("bad window: blk %d tid %d k %d l %d lo %d w %d s %.17g\n", blockIdx.x, threadIdx.x, kk, ll, sh_lo[kk],
+             sh_base[kk + 1] - sh_base[kk], s);
+#endif
     pm = mat[j];
     load_q<GP>(qt, j, pq);
   }
+  __device__ __forceinline__ int first_cell() const { return sh_kinfo[fkl & 0xffff].y + (fkl >> 16); }
 };
 
-// forward OTF: advance until the pending segment belongs to a chunk >= k_hi (or the end)
+// forward OTF: advance until the pending segment's cell is >= c_hi (a later chunk) or
+// the track ends
 template <int G, int GP>
 __device__ __forceinline__ void walk_fwd_chunk(WalkState<GP>& w, Physics<G, GP>& ph, double z0, double tn,
-                                               double isn, bool up, int k_hi) {
+                                               double isn, int dl, int po, int c_hi) {
   while (true) {
-    if (w.have && w.pk >= k_hi) return;
+    if (w.pc >= c_hi) return;
     if (w.done) {
-      if (w.have) {
-        ph.emit(w.pk, w.pl, w.pm, w.pq, w.pL);
-        w.have = false;
+      if (w.pc >= 0) {
+        ph.emit(w.pc, w.pm, w.pq, w.pL);
+        w.pc = -1;
+        w.fkl = -1;  // the track is finished: no all-sliver emission follows
+      } else if (w.fkl >= 0) {  // all-sliver track: one segment at its first piece
+        if (w.first_cell() >= c_hi) return;
+#ifdef MOC_DEBUG_WALK
+        printf("all-sliver fwd: blk %d tid %d fkl k %d l %d first_cell %d chunk [%d,%d) s %.17g s_end %.17g carry %g\n",
+               blockIdx.x, threadIdx.x, w.fkl & 0xffff, w.fkl >> 16, w.first_cell(), ph.dbg_lo, c_hi, w.s, w.s_end,
+               w.carry);
+#endif
+        w.set_pending(w.fkl & 0xffff, w.fkl >> 16, ph.mat, ph.qt);
+        ph.emit(w.pc, w.pm, w.pq, w.carry);
+        w.pc = -1;
+        w.fkl = -1;
       }
       return;
     }
-    const double s_rad = sh_send[w.k];
-    const double s_ax = (sh_planes[up ? w.l + 1 : w.l] - z0) * tn;
-    double s_next = s_rad < s_ax ? s_rad : s_ax;
-    s_next = s_next < w.s_end ? s_next : w.s_end;
-    const double L3d = (s_next - w.s) * isn;
+    const bool rad = w.s_rad <= w.s_ax;
+    double sn = rad ? w.s_rad : w.s_ax;
+    const bool last = sn >= w.s_end;
+    sn = last ? w.s_end : sn;
+    const double L3d = (sn - w.s) * isn;
     const float L3 = (float)L3d;
     if (L3d < kEpsL) {
-      if (w.have) {
-        w.pL += L3;
+      if (w.pc >= 0) {
+        w.pL += L3;  // a sliver merges into the segment before it
       } else {
-        w.pL = L3;
-        w.lead = true;
-        w.have = true;
-        w.set_pending(w.k, w.l, ph.mat, ph.qt);
+        w.carry += L3;  // a leading sliver run merges forward
+        if (w.fkl < 0) w.fkl = w.k | (w.l << 16);
       }
     } else {
-      if (w.have && !w.lead) ph.emit(w.pk, w.pl, w.pm, w.pq, w.pL);
-      w.pL = (w.have && w.lead) ? w.pL + L3 : L3;  // a leading sliver run merges forward
-      w.lead = false;
-      w.have = true;
+      if (w.pc >= 0) ph.emit(w.pc, w.pm, w.pq, w.pL);
+      w.pL = L3 + w.carry;
+      w.carry = 0.f;
       w.set_pending(w.k, w.l, ph.mat, ph.qt);
     }
-    if (s_next >= w.s_end) {
+    if (last) {
       w.done = true;
     } else {
-      if (s_rad <= s_ax) ++w.k; else w.l += up ? 1 : -1;
-      w.s = s_next;
+      w.s = sn;
+#ifdef MOC_V2_BRANCHY
+      if (rad) {
+        ++w.k;
+        w.s_rad = sh_sendx[w.k + 1];
+      } else {
+        w.l += dl;
+        w.s_ax = (sh_planes[w.l + po] - z0) * tn;
+      }
+#else
+      w.k += rad ? 1 : 0;
+      w.l += rad ? 0 : dl;
+      w.s_rad = sh_sendx[w.k + 1];
+      w.s_ax = (sh_planes[w.l + po] - z0) * tn;
+#endif
     }
   }
 }
 
-// backward OTF: retreat until the pending segment belongs to a chunk < k_lo (or the
-// start).  Short raw pieces are carried into the next long one, so the merged list is
-// the reverse of the forward one (reading Q22b).
+// backward OTF: retreat until the pending segment's cell is < c_lo (an earlier chunk)
+// or the track start.  Short raw pieces are carried into the next long one, so the
+// merged list is the reverse of the forward one (reading Q22b).
 template <int G, int GP>
 __device__ __forceinline__ void walk_bwd_chunk(WalkState<GP>& w, Physics<G, GP>& ph, double z0, double tn,
-                                               double isn, bool up, int k_lo) {
+                                               double isn, int dl, int po, int c_lo) {
   while (true) {
-    if (w.have && w.pk < k_lo) return;
+    if ((unsigned)w.pc < (unsigned)c_lo) return;
     if (w.done) {
-      if (w.have) {
-        ph.emit(w.pk, w.pl, w.pm, w.pq, w.pL + w.carry);
-        w.have = false;
-        w.pk = -1;
-      } else if (w.pk >= 0) {
-        if (w.pk < k_lo) return;  // all-sliver track: emit in the chunk of its last raw piece
-        w.set_pending(w.pk, w.pl, ph.mat, ph.qt);
-        ph.emit(w.pk, w.pl, w.pm, w.pq, w.carry);
-        w.pk = -1;
+      if (w.pc >= 0) {
+        ph.emit(w.pc, w.pm, w.pq, w.pL + w.carry);
+        w.pc = -1;
+        w.fkl = -1;  // the track is finished: no all-sliver emission follows
+      } else if (w.fkl >= 0) {  // all-sliver track: emitted in the chunk of its first piece
+        if (w.first_cell() < c_lo) return;
+        w.set_pending(w.fkl & 0xffff, w.fkl >> 16, ph.mat, ph.qt);
+        ph.emit(w.pc, w.pm, w.pq, w.carry);
+        w.pc = -1;
+        w.fkl = -1;
       }
       return;
     }
-    const double s_rad = w.k > 0 ? sh_send[w.k - 1] : 0.0;
-    const double s_ax = (sh_planes[up ? w.l : w.l + 1] - z0) * tn;
-    double s_prev = s_rad > s_ax ? s_rad : s_ax;
-    s_prev = s_prev > w.s_end ? s_prev : w.s_end;
-    const double L3d = (w.s - s_prev) * isn;
+    const bool rad = w.s_rad >= w.s_ax;
+    double sp = rad ? w.s_rad : w.s_ax;
+    const bool last = sp <= w.s_end;
+    sp = last ? w.s_end : sp;
+    const double L3d = (w.s - sp) * isn;
     const float L3 = (float)L3d;
     if (L3d < kEpsL) {
       w.carry += L3;
-      if (!w.have) {
-        w.pk = w.k;  // remembered for the all-sliver case only
-        w.pl = w.l;
-      }
+      if (w.pc < 0) w.fkl = w.k | (w.l << 16);  // the forward-first sliver wins
     } else {
-      if (w.have) ph.emit(w.pk, w.pl, w.pm, w.pq, w.pL);
+      if (w.pc >= 0) ph.emit(w.pc, w.pm, w.pq, w.pL);
       w.pL = L3 + w.carry;
       w.carry = 0.f;
-      w.have = true;
       w.set_pending(w.k, w.l, ph.mat, ph.qt);
     }
-    if (s_prev <= w.s_end) {
+    if (last) {
       w.done = true;
     } else {
-      if (s_rad >= s_ax) --w.k; else w.l -= up ? 1 : -1;
-      w.s = s_prev;
+      w.s = sp;
+#ifdef MOC_V2_BRANCHY
+      if (rad) {
+        --w.k;
+        w.s_rad = sh_sendx[w.k];
+      } else {
+        w.l -= dl;
+        w.s_ax = (sh_planes[w.l + 1 - po] - z0) * tn;
+      }
+#else
+      w.k -= rad ? 1 : 0;
+      w.l -= rad ? 0 : dl;
+      w.s_rad = sh_sendx[w.k];
+      w.s_ax = (sh_planes[w.l + 1 - po] - z0) * tn;
+#endif
     }
   }
 }
@@ -278,6 +357,7 @@ struct Replay {
   const Rec* rs;
   int q, qend, dq;  // next record to apply; stop index (exclusive)
   Rec cur;
+  int cpc;
   float cq[GP];
   bool valid;
 
@@ -286,7 +366,9 @@ struct Replay {
     if (valid) {
       cur = rs[(size_t)q * kV2Threads];
       const int kk = cur.meta & 1023, l = (cur.meta >> 10) & 255;
-      load_q<GP>(qt, (int64_t)(sh_kinfo[kk].x + l), cq);
+      const int2 ki = sh_kinfo[kk];
+      cpc = ki.y + l;
+      load_q<GP>(qt, (int64_t)(ki.x + l), cq);
     }
   }
 };
@@ -297,14 +379,14 @@ __device__ __forceinline__ void replay_chunk(Replay<GP>& r, Physics<G, GP>& ph, 
   while (r.valid) {
     const int kk = r.cur.meta & 1023;
     if (kk < k_lo || kk >= k_hi) return;
-    const int l = (r.cur.meta >> 10) & 255, m = r.cur.meta >> 18;
+    const int m = r.cur.meta >> 18, pc = r.cpc;
     const float L = r.cur.L;
     float q[GP];
 #pragma unroll
     for (int h = 0; h < GP; ++h) q[h] = r.cq[h];
     r.q += r.dq;
     r.fetch(ph.qt);  // look-ahead load overlaps the physics below
-    ph.emit(kk, l, m, q, L);
+    ph.emit(pc, m, q, L);
   }
 }
 
@@ -329,6 +411,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
   constexpr int stride = GP + 1;
   const int cap_cells = a.tile_words / stride;
   double leak = 0.0;
+  uint64_t nemit = 0;  // merged segment-direction emissions flushed by this thread
 
   while (true) {
     __syncthreads();
@@ -346,12 +429,12 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const double dz = d.an_dz[an], cot = d.an_cot[an];
     const double z0b = d.st_z0[s];
     const double zf = z0b + (double)U.i0 * dz, zl = z0b + (double)(U.i0 + U.n - 1) * dz;
-    const OtfView v{sh_send, sh_reg, sh_planes, d.NL};
+    const OtfView v{sh_sendx + 1, sh_reg, sh_planes, d.NL};
     // 1-2. stage the 2D segments, per-k layer windows of the band
     for (int kk = tid; kk < nk; kk += blockDim.x) {
       const double s1 = d.seg_send[sb + kk];
       const double s0 = kk ? d.seg_send[sb + kk - 1] : 0.0;
-      sh_send[kk] = s1;
+      sh_sendx[kk + 1] = s1;
       sh_reg[kk] = d.seg_region[sb + kk];
       double zlo = cot > 0 ? zf + s0 * cot : zf + s1 * cot;
       double zhi = cot > 0 ? zl + s1 * cot : zl + s0 * cot;
@@ -366,6 +449,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
       sh_base[kk] = w;
     }
     if (tid < kMaxG) sh_max[tid] = 0u;
+    if (tid == 0) sh_sendx[0] = 0.0;
     __syncthreads();
     if (warp == 0) {
       int carry = 0;
@@ -404,21 +488,16 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         s_nchunk = nc;
       }
     }
-    // 3. one track per thread; lanes of a warp are `nact` members apart
-    const int nact = ((int)U.n + 31) >> 5;  // warps with work
-    const int p = lane * nact + warp;
-    const bool active = warp < nact && p < (int)U.n;
+    // 3. one track per thread (member_of: neighbouring members share a warp)
+    const int p = member_of(tid, lane_lg_of(dz, a.h_lane, a.lane_lg, (int)U.n));
+    const bool active = p < (int)U.n;
     const uint32_t id = d.st_first[s] + U.i0 + (uint32_t)p;
     Physics<G, GP> ph;
-    float pb[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      ph.psi[g] = active ? a.psi_in[(size_t)(2 * id) * GP + g] * ps : 0.f;
-      pb[g] = active ? a.psi_in[(size_t)(2 * id + 1) * GP + g] * ps : 0.f;
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float m = fmaxf(ph.psi[g], pb[g]);
+      const float f = active ? a.psi_in[(size_t)(2 * id) * GP + g] * ps : 0.f;
+      const float b = active ? a.psi_in[(size_t)(2 * id + 1) * GP + g] * ps : 0.f;
+      float m = fmaxf(f, b);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
       if (lane == 0) atomicMax(&sh_max[g], __float_as_uint(m));
@@ -435,10 +514,10 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     for (int g = 0; g < G; ++g) ph.scl[g] = sh_scale[g];
     ph.mat = a.mat;
     ph.qt = a.qt;
-    ph.tile = tile;
     const double tn = d.an_tan[an], isn = d.an_invsin[an], Lt = d.t_len[t];
     const double z0 = z0b + (double)(U.i0 + p) * dz;
     const bool up = cot > 0;
+    const int dl = up ? 1 : -1, po = up ? 1 : 0;
     const float cw = d.an_c[an];
     const bool otf = !HYBRID || exp_off == kNoExp;
     double s_in = 0, s_out = 0;
@@ -456,19 +535,17 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     }
 #pragma unroll 1
     for (int dir = 0; dir < 2; ++dir) {
-      if (dir == 1) {
 #pragma unroll
-        for (int g = 0; g < G; ++g) ph.psi[g] = pb[g];
-      }
+      for (int g = 0; g < G; ++g)
+        ph.psi[g] = active ? a.psi_in[(size_t)(2 * id + dir) * GP + g] * ps * ph.scl[g] : 0.f;
       WalkState<GP> w;
       Replay<GP> r;
       if (otf) {
-        w.have = false;
-        w.lead = false;
         w.done = !active;
         w.carry = 0.f;
-        w.pk = -1;
-        w.pl = 0;
+        w.pc = -1;
+        w.pm = 0;
+        w.fkl = -1;
         w.pL = 0.f;
         if (dir == 0) {
           w.s = s_in;
@@ -492,6 +569,8 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
             w.k = nk - 1;
           }
         }
+        w.s_rad = active ? sh_sendx[dir == 0 ? w.k + 1 : w.k] : 0.0;
+        w.s_ax = active ? (sh_planes[dir == 0 ? w.l + po : w.l + 1 - po] - z0) * tn : 0.0;
       } else {
         // EXP: this thread's preloaded records, first to last or last to first
         const int nrec = active ? (int)a.cost[id] : 0;
@@ -506,10 +585,15 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const int c = dir == 0 ? ci : nchunk - 1 - ci;
         const int k_lo = sh_chunk[c], k_hi = sh_chunk[c + 1];
         const int cb = sh_base[k_lo];
-        ph.cbase = cb;
+        ph.ctile = tile - cb * stride;
+#ifdef MOC_DEBUG_WALK
+        ph.dbg_lo = cb;
+        ph.dbg_hi = sh_base[k_hi];
+        ph.dbg_dir = dir;
+#endif
         if (!otf) replay_chunk(r, ph, k_lo, k_hi);
-        else if (dir == 0) walk_fwd_chunk(w, ph, z0, tn, isn, up, k_hi);
-        else walk_bwd_chunk(w, ph, z0, tn, isn, up, k_lo);
+        else if (dir == 0) walk_fwd_chunk(w, ph, z0, tn, isn, dl, po, sh_base[k_hi]);
+        else walk_bwd_chunk(w, ph, z0, tn, isn, dl, po, cb);
         __syncthreads();
         // 4. flush the chunk: c_{a,n} * fixed-point sums -> global tally (fp32 vector
         //    reductions), re-zeroing every consumed cell for the next chunk
@@ -520,6 +604,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
             uint32_t* cell = tile + (b + x) * stride;
             const uint32_t cnt = cell[GP];
             if (!cnt) continue;
+            nemit += cnt;
             float val[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) {
@@ -544,34 +629,36 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const uint32_t out = a.link[2 * id + dir];
         if (out != 0xffffffffu) {
 #pragma unroll
-          for (int g = 0; g < G; ++g) a.psi_out[(size_t)out * GP + g] = ph.psi[g];
+          for (int g = 0; g < G; ++g) a.psi_out[(size_t)out * GP + g] = ph.psi[g] * sh_iscale[g];
         } else {
           float e = 0.f;
 #pragma unroll
-          for (int g = 0; g < G; ++g) e += ph.psi[g];
+          for (int g = 0; g < G; ++g) e += ph.psi[g] * sh_iscale[g];
           leak += (double)(cw * e);
         }
       }
     }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) leak += __shfl_xor_sync(0xffffffffu, leak, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    leak += __shfl_xor_sync(0xffffffffu, leak, o);
+    nemit += __shfl_xor_sync(0xffffffffu, nemit, o);
+  }
   if (lane == 0 && leak != 0.0) atomicAdd(&a.sc[SC_LEAK], leak);
+  if (lane == 0 && nemit) atomicAdd(&a.sc[SC_NEMIT], (double)nemit);
 }
 
 // EXP preload ("the device function for generating characteristic lines is
 // executed, and these data are stored on the GPU"): walk every track of a preloaded
 // unit once and store its merged segments as records, lane-interleaved per unit.
 __global__ void k_exp_generate(DevData d, const Unit* units, const uint64_t* unit_exp, uint32_t n_units,
-                               const uint8_t* mat, Rec* store) {
+                               const uint8_t* mat, Rec* store, double h_lane, int lane_lg) {
   const OtfView v = dev_view(d);
   for (uint32_t u = blockIdx.x; u < n_units; u += gridDim.x) {
     if (unit_exp[u] == kNoExp) continue;
     const Unit U = units[u];
-    const int nact = ((int)U.n + 31) >> 5;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int p = lane * nact + warp;
-    if (warp >= nact || p >= (int)U.n) continue;
+    const int p = member_of(threadIdx.x, lane_lg_of(d.an_dz[d.t_a[U.stack / d.N] * d.N + U.stack % d.N], h_lane, lane_lg, (int)U.n));
+    if (p >= (int)U.n) continue;
     int s, an;
     const uint32_t id = d.st_first[U.stack] + U.i0 + (uint32_t)p;
     TrackGeo g = dev_track(d, id, s, an);

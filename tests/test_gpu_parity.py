@@ -22,6 +22,13 @@ def M():
     return mod
 
 
+def _check_emitted(s):
+    """Integrity counter: every merged 3D segment was applied exactly once per direction
+    in the last sweep (no lost or phantom emissions at chunk boundaries)."""
+    t = s.timings()
+    assert t["emitted_last"] == 2 * t["n_segs3d"], (t["emitted_last"], t["n_segs3d"])
+
+
 def _flux_err(phi, ref):
     linf = np.abs(phi - ref).max() / np.abs(ref).max()
     mask = ref >= 1e-6 * ref.max()
@@ -54,6 +61,7 @@ def test_fixed_iteration_parity_small_lattice(M, oracle_mod, schedule):
     prob = P.small_lattice(3, 3, 4)
     s = M.Solver(M.Problem(prob), schedule=schedule)
     k, _ = s.iterate(8)
+    _check_emitted(s)
     ref = oracle_mod.Oracle(prob).solve(fixed_iters=8)
     assert k == pytest.approx(ref["k"], abs=1e-5)
     linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
@@ -69,6 +77,7 @@ def test_many_chunk_tiles_parity(M, oracle_mod, tile_cells):
     prob = P.small_lattice(3, 3, 4)
     s = M.Solver(M.Problem(prob), tile_cells=tile_cells)
     k, _ = s.iterate(6)
+    _check_emitted(s)
     ref = oracle_mod.Oracle(prob).solve(fixed_iters=6)
     assert k == pytest.approx(ref["k"], abs=1e-5)
     linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
@@ -90,6 +99,7 @@ def test_exp_preload_parity(M, oracle_mod, budget_mb):
     else:
         assert t["exp_segments"] == t["n_segs3d"]
     k, _ = s.iterate(3)
+    _check_emitted(s)
     ref = oracle_mod.Oracle(prob).solve(fixed_iters=3)
     assert k == pytest.approx(ref["k"], abs=1e-5)
     linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
@@ -156,6 +166,7 @@ def test_full_size_fixed_iteration_parity(M, oracle_mod, cfg, iters):
     prob = P.config(cfg)
     s = M.Solver(M.Problem(prob))
     k, _ = s.iterate(iters)
+    _check_emitted(s)
     ref = oracle_mod.Oracle(prob).solve(fixed_iters=iters)
     assert k == pytest.approx(ref["k"], abs=1e-5)
     linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
@@ -170,6 +181,7 @@ def test_cfg3_reduced_fixed_iterations(M, oracle_mod):
     prob = P.with_quadrature(P.config(3), num_azim=8, num_polar=4, radial_spacing=0.5, axial_spacing=3.0)
     s = M.Solver(M.Problem(prob))
     k, _ = s.iterate(3)
+    _check_emitted(s)
     ref = oracle_mod.Oracle(prob).solve(fixed_iters=3)
     assert k == pytest.approx(ref["k"], abs=1e-5)
     linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
