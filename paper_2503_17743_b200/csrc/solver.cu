@@ -196,6 +196,7 @@ __global__ void k_source(int64_t J, const uint8_t* mat, const float* phi, const 
       for (int h = 0; h < G; ++h) s = fmaf(c_sigs[(m * kMaxG + h) * kMaxG + g], ph[h], s);
       qt[j * GP + g] = s / ((float)kFourPi * c_sigt[m * kMaxG + g]);
     }
+    if constexpr (G < GP) qt[j * GP + G] = __int_as_float(m);  // material for the v2 sweep's prefetch
     fold[j] = F;
     acc += vol[j] * (double)F;
   }
@@ -506,7 +507,7 @@ struct moc_solver {
   uint32_t* d_counter = nullptr;
   float *d_rmax = nullptr, *d_qmax_t = nullptr, *d_tally32 = nullptr;
   int* d_err = nullptr;
-  int tile_words = 0;
+  int cap_cells = 0;  // forced tile cap in cells (moc_solver_opts.tile_cells), 0 = none
   int lane_lg = -1;  // forced log2 v2 lane stride (MOC_V2_LANE_STRIDE), -1 = per unit
   double h_lane = 0;     // thinnest axial layer / 3 (sweep_v2.cuh lane_lg_of)
   size_t v2_smem = 0;
@@ -579,7 +580,8 @@ void run_sweep(moc_solver* s) {
     a.psi_out = s->d_psi[out];
     a.tally = s->d_tally32;
     a.sc = s->d_sc;
-    a.tile_words = s->tile_words;
+    a.dyn_bytes = (int)s->v2_smem;
+    a.cap_cells = s->cap_cells;
     a.lane_lg = s->lane_lg;
     a.h_lane = s->h_lane;
     a.err = s->d_err;
@@ -605,7 +607,6 @@ void v2_configure(moc_solver* s) {
   CUDA_OK(cudaFuncGetAttributes(&fb, k_sweep_v2<G, GP, true>));
   const size_t per_cta = (228 * 1024) / kV2MinBlocks - 1024;
   s->v2_smem = (per_cta - std::max(fa.sharedSizeBytes, fb.sharedSizeBytes)) & ~size_t(15);
-  s->tile_words = (int)(s->v2_smem / 4);
   CUDA_OK(cudaFuncSetAttribute(k_sweep_v2<G, GP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)s->v2_smem));
   CUDA_OK(cudaFuncSetAttribute(k_sweep_v2<G, GP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -953,14 +954,17 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     if (sched < 0 || sched > 2) throw Error(MOC_E_INVALID_ARG, "schedule must be 0, 1 or 2");
     if (sched == 0) {
       // persistent stack-band units (sweep_v2.cuh), sorted by exact segment count descending
-      for (int64_t t = 0; t < s->T2; ++t)
-        if (L.t_seg[t + 1] - L.t_seg[t] > kMaxK) throw Error(MOC_E_CAPACITY, "2D track with more than 512 segments");
+      int64_t max_nk = 0;
+      for (int64_t t = 0; t < s->T2; ++t) max_nk = std::max(max_nk, L.t_seg[t + 1] - L.t_seg[t]);
+      if (max_nk > kMaxK) throw Error(MOC_E_CAPACITY, "2D track with more than 512 segments");
       if (g.NL + 1 > kMaxPlanes) throw Error(MOC_E_CAPACITY, "more than 255 axial layers");
-      v2_configure_any(s);  // tile size from the kernel's static shared footprint
-      if (s->tile_words / (s->GP + 1) < 2 * g.NL) throw Error(MOC_E_CAPACITY, "axial mesh too fine for the tally tile");
+      v2_configure_any(s);  // dynamic shared memory from the kernel's static footprint
+      // the tile left below the largest unit's tables must hold two full layer columns
+      if (((int64_t)s->v2_smem - unit_table_bytes((int)max_nk)) / (4 * (s->GP + 1)) < 2 * g.NL)
+        throw Error(MOC_E_CAPACITY, "axial mesh too fine for the tally tile");
       if (s->opts.tile_cells > 0) {
         if (s->opts.tile_cells < g.NL) throw Error(MOC_E_PARAM, "tile_cells must be >= the number of axial layers");
-        s->tile_words = std::min(s->tile_words, s->opts.tile_cells * (s->GP + 1));
+        s->cap_cells = s->opts.tile_cells;
       }
       {
         double hmin = 1e300;

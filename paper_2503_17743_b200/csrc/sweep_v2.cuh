@@ -44,18 +44,25 @@ constexpr float kMagic = 12582912.0f;         // 1.5 * 2^23
 constexpr float kFixOne = 2097152.0f;         // 2^21: max |term| in fixed point
 constexpr uint64_t kNoExp = ~0ull;            // unit not preloaded (on-the-fly)
 
-// per-unit shared tables
-__shared__ double sh_sendx[kMaxK + 1];   // [0] = 0, [k + 1] = cumulative end of 2D segment k
-__shared__ double sh_planes[kMaxPlanes]; // axial planes
-__shared__ int2 sh_kinfo[kMaxK];         // {region * NL, first tile cell of k - lo_k}
-__shared__ uint32_t sh_reg[kMaxK];
-__shared__ int sh_lo[kMaxK];
-__shared__ int sh_base[kMaxK + 4];
-__shared__ int sh_chunk[kMaxK + 4];
+// per-kernel shared tables; the per-unit tables share the dynamic buffer with the tile
+__shared__ double sh_planes[kMaxPlanes];  // axial planes
 __shared__ __align__(16) float sh_sig[kMaxMat * kMaxG];  // sigma_t * log2(e), [m][GP]
 __shared__ float sh_iscale[kMaxG];
 __shared__ float sh_scale[kMaxG];
 __shared__ unsigned sh_max[kMaxG];
+
+// Per 2D segment k of the unit's 2D track, one 16-byte record per walk direction: the
+// crossing the walk meets next in k (forward table: s at the end of k; backward table:
+// s at its start) with k's FSR and tile-cell offsets, so a radial step is one LDS.128.
+struct __align__(16) KSeg {
+  double s;
+  int kx;  // region(k) * NL: FSR j = kx + layer
+  int ky;  // first tile cell of k - lo_k: cell = ky + layer
+};
+
+// Dynamic shared memory of one CTA: [tile cells ... | TF[nk] | TB[nk] | base[nk+1] |
+// chunk[nk+1]]; the tables are sized per unit from the top, the tile takes the rest.
+__host__ __device__ constexpr int unit_table_bytes(int nk) { return 32 * nk + ((8 * (nk + 1) + 15) & ~15); }
 
 struct Unit {
   uint32_t stack, i0, n, cost;
@@ -78,7 +85,7 @@ struct V2Args {
   uint32_t* counter;
   const uint32_t* link;
   const uint8_t* mat;
-  const float* qt;
+  const float* qt;      // [J][GP]; for G < GP slot G carries the FSR's material index bits
   const float* qmax_t;  // [T2][GP] max qtilde over the FSRs under 2D track t
   const float* psi_in;
   float* psi_out;
@@ -86,8 +93,9 @@ struct V2Args {
   double* sc;
   const Rec* store;     // EXP record store
   const uint32_t* cost; // exact merged segments per track (EXP replay length)
-  int tile_words;
-  double h_lane;            // thinnest axial layer / 3 (lane_lg_of)
+  int dyn_bytes;        // dynamic shared memory per CTA
+  int cap_cells;        // tile cap in cells (tests force many chunks), <= 0: none
+  double h_lane;        // thinnest axial layer / 3 (lane_lg_of)
   int lane_lg;          // forced log2 lane stride, -1 = per unit (lane_lg_of)
   int* err;
 };
@@ -143,6 +151,25 @@ __device__ __forceinline__ void load_q(const float* qt, int64_t j, float* q) {
   }
 }
 
+// first k in [0, nk-1] with T[k].s > s  /  >= s  (otf_seg_after / otf_seg_upto on the
+// forward table, whose s is the cumulative end of each 2D segment)
+__device__ __forceinline__ int kseg_after(const KSeg* T, int nk, double s) {
+  int lo = 0, hi = nk - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (T[mid].s > s) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+__device__ __forceinline__ int kseg_upto(const KSeg* T, int nk, double s) {
+  int lo = 0, hi = nk - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (T[mid].s >= s) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
 // Eq. 3 + Eq. 4 for one merged segment in all groups.  psi is carried in the unit's
 // fixed-point units (psi' = psi * scale_g, scale_g = 2^21 / bound_g), so the tally term
 // dpsi' = (psi' - q scale_g)(1 - e^{-tau}) is already scaled and its fixed-point code is
@@ -154,15 +181,15 @@ struct Physics {
   const uint8_t* mat;
   const float* qt;
   uint32_t* ctile;  // tile - (first cell of the current chunk) * (GP + 1)
-
 #ifdef MOC_DEBUG_WALK
-  int dbg_lo, dbg_hi, dbg_dir, dbg_k, dbg_l;
+  int dbg_lo, dbg_hi, dbg_dir;
 #endif
+
   __device__ __forceinline__ void emit(int pc, int m, const float* q, float Lf) {
 #ifdef MOC_DEBUG_WALK
     if (pc < dbg_lo || pc >= dbg_hi) {
-      printf("bad emit: blk %d tid %d dir %d pc %d chunk [%d,%d) k %d l %d m %d L %g\n", blockIdx.x, threadIdx.x,
-             dbg_dir, pc, dbg_lo, dbg_hi, dbg_k, dbg_l, m, Lf);
+      printf("bad emit: blk %d tid %d dir %d pc %d chunk [%d,%d) m %d L %g\n", blockIdx.x, threadIdx.x, dbg_dir, pc,
+             dbg_lo, dbg_hi, m, Lf);
       return;
     }
 #endif
@@ -194,40 +221,40 @@ struct Physics {
 };
 
 // On-the-fly walk state (same piece and merge rules as otf.h, reading Q22b).  The
-// next radial and axial crossings are cached (s_rad, s_ax) and refreshed only for the
-// boundary just crossed.  Pending merged segment: pc = its tile cell index (-1 = none;
-// cells of 2D segment k are [base_k, base_k+1), so chunk membership is a compare on
-// pc), pm / pq = material and source loaded when it was set (one raw piece ahead of
-// use).  carry = sliver length not yet attached to a long piece; fkl = first sliver
-// (k | l << 16) seen while nothing is pending (all-sliver tracks only, else -1).
-template <int GP>
+// next radial and axial crossings are cached (s_rad with k's offsets kx / ky from one
+// KSeg load, s_ax) and refreshed after each step.  Pending merged segment: pc = its
+// tile cell (-1 = none; cells of 2D segment k are [base_k, base_k+1), so chunk
+// membership is a compare on pc), pm / pq = material and source loaded when it was set
+// (one raw piece ahead of use).  carry = sliver length not yet attached to a long
+// piece; fkl = first sliver (k | l << 16) seen while nothing is pending (all-sliver
+// tracks only, else -1).
+template <int G, int GP>
 struct WalkState {
   double s, s_end, s_rad, s_ax;
-  int k, l, pc, pm, fkl;
+  int k, l, kx, ky, pc, pm, fkl, done;
   float pL, carry;
-  bool done;
   float pq[GP];
 
-  __device__ __forceinline__ void set_pending(int kk, int ll, const uint8_t* mat, const float* qt) {
-    const int2 ki = sh_kinfo[kk];
-    const int64_t j = (int64_t)(ki.x + ll);
-    pc = ki.y + ll;
-#ifdef MOC_DEBUG_WALK
-    if (pc < sh_base[kk] || pc >= sh_base[kk + 1])
-      printf("bad window: blk %d tid %d k %d l %d lo %d w %d s %.17g\n", blockIdx.x, threadIdx.x, kk, ll, sh_lo[kk],
-             sh_base[kk + 1] - sh_base[kk], s);
-#endif
-    pm = mat[j];
-    load_q<GP>(qt, j, pq);
+  __device__ __forceinline__ void load(const KSeg& e) {
+    s_rad = e.s;
+    kx = e.kx;
+    ky = e.ky;
   }
-  __device__ __forceinline__ int first_cell() const { return sh_kinfo[fkl & 0xffff].y + (fkl >> 16); }
+  // make raw piece (k, l) the pending segment: its cell, source and material
+  __device__ __forceinline__ void set_pending(int jx, int cy, int ll, const uint8_t* mat, const float* qt) {
+    const int64_t j = (int64_t)(jx + ll);
+    pc = cy + ll;
+    load_q<GP>(qt, j, pq);
+    if constexpr (G < GP) pm = __float_as_int(pq[G]);  // material index rides in the pad slot
+    else pm = mat[j];
+  }
 };
 
 // forward OTF: advance until the pending segment's cell is >= c_hi (a later chunk) or
-// the track ends
-template <int G, int GP>
-__device__ __forceinline__ void walk_fwd_chunk(WalkState<GP>& w, Physics<G, GP>& ph, double z0, double tn,
-                                               double isn, int dl, int po, int c_hi) {
+// the track ends.  UP: the track climbs (cot > 0).
+template <int G, int GP, bool UP>
+__device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, GP>& ph, const KSeg* TF, double z0,
+                                               double tn, double isn, int c_hi) {
   while (true) {
     if (w.pc >= c_hi) return;
     if (w.done) {
@@ -236,13 +263,9 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<GP>& w, Physics<G, GP>&
         w.pc = -1;
         w.fkl = -1;  // the track is finished: no all-sliver emission follows
       } else if (w.fkl >= 0) {  // all-sliver track: one segment at its first piece
-        if (w.first_cell() >= c_hi) return;
-#ifdef MOC_DEBUG_WALK
-        printf("all-sliver fwd: blk %d tid %d fkl k %d l %d first_cell %d chunk [%d,%d) s %.17g s_end %.17g carry %g\n",
-               blockIdx.x, threadIdx.x, w.fkl & 0xffff, w.fkl >> 16, w.first_cell(), ph.dbg_lo, c_hi, w.s, w.s_end,
-               w.carry);
-#endif
-        w.set_pending(w.fkl & 0xffff, w.fkl >> 16, ph.mat, ph.qt);
+        const KSeg e = TF[w.fkl & 0xffff];
+        if (e.ky + (w.fkl >> 16) >= c_hi) return;
+        w.set_pending(e.kx, e.ky, w.fkl >> 16, ph.mat, ph.qt);
         ph.emit(w.pc, w.pm, w.pq, w.carry);
         w.pc = -1;
         w.fkl = -1;
@@ -266,25 +289,25 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<GP>& w, Physics<G, GP>&
       if (w.pc >= 0) ph.emit(w.pc, w.pm, w.pq, w.pL);
       w.pL = L3 + w.carry;
       w.carry = 0.f;
-      w.set_pending(w.k, w.l, ph.mat, ph.qt);
+      w.set_pending(w.kx, w.ky, w.l, ph.mat, ph.qt);
     }
     if (last) {
-      w.done = true;
+      w.done = 1;
     } else {
       w.s = sn;
-#ifdef MOC_V2_BRANCHY
+#ifndef MOC_V2_BRANCHLESS
       if (rad) {
         ++w.k;
-        w.s_rad = sh_sendx[w.k + 1];
+        w.load(TF[w.k]);
       } else {
-        w.l += dl;
-        w.s_ax = (sh_planes[w.l + po] - z0) * tn;
+        w.l += UP ? 1 : -1;
+        w.s_ax = (sh_planes[w.l + (UP ? 1 : 0)] - z0) * tn;
       }
 #else
       w.k += rad ? 1 : 0;
-      w.l += rad ? 0 : dl;
-      w.s_rad = sh_sendx[w.k + 1];
-      w.s_ax = (sh_planes[w.l + po] - z0) * tn;
+      w.l += rad ? 0 : (UP ? 1 : -1);
+      w.load(TF[w.k]);
+      w.s_ax = (sh_planes[w.l + (UP ? 1 : 0)] - z0) * tn;
 #endif
     }
   }
@@ -293,9 +316,9 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<GP>& w, Physics<G, GP>&
 // backward OTF: retreat until the pending segment's cell is < c_lo (an earlier chunk)
 // or the track start.  Short raw pieces are carried into the next long one, so the
 // merged list is the reverse of the forward one (reading Q22b).
-template <int G, int GP>
-__device__ __forceinline__ void walk_bwd_chunk(WalkState<GP>& w, Physics<G, GP>& ph, double z0, double tn,
-                                               double isn, int dl, int po, int c_lo) {
+template <int G, int GP, bool UP>
+__device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, GP>& ph, const KSeg* TF,
+                                               const KSeg* TB, double z0, double tn, double isn, int c_lo) {
   while (true) {
     if ((unsigned)w.pc < (unsigned)c_lo) return;
     if (w.done) {
@@ -304,8 +327,9 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<GP>& w, Physics<G, GP>&
         w.pc = -1;
         w.fkl = -1;  // the track is finished: no all-sliver emission follows
       } else if (w.fkl >= 0) {  // all-sliver track: emitted in the chunk of its first piece
-        if (w.first_cell() < c_lo) return;
-        w.set_pending(w.fkl & 0xffff, w.fkl >> 16, ph.mat, ph.qt);
+        const KSeg e = TF[w.fkl & 0xffff];
+        if (e.ky + (w.fkl >> 16) < c_lo) return;
+        w.set_pending(e.kx, e.ky, w.fkl >> 16, ph.mat, ph.qt);
         ph.emit(w.pc, w.pm, w.pq, w.carry);
         w.pc = -1;
         w.fkl = -1;
@@ -325,25 +349,25 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<GP>& w, Physics<G, GP>&
       if (w.pc >= 0) ph.emit(w.pc, w.pm, w.pq, w.pL);
       w.pL = L3 + w.carry;
       w.carry = 0.f;
-      w.set_pending(w.k, w.l, ph.mat, ph.qt);
+      w.set_pending(w.kx, w.ky, w.l, ph.mat, ph.qt);
     }
     if (last) {
-      w.done = true;
+      w.done = 1;
     } else {
       w.s = sp;
-#ifdef MOC_V2_BRANCHY
+#ifndef MOC_V2_BRANCHLESS
       if (rad) {
         --w.k;
-        w.s_rad = sh_sendx[w.k];
+        w.load(TB[w.k]);
       } else {
-        w.l -= dl;
-        w.s_ax = (sh_planes[w.l + 1 - po] - z0) * tn;
+        w.l -= UP ? 1 : -1;
+        w.s_ax = (sh_planes[w.l + (UP ? 0 : 1)] - z0) * tn;
       }
 #else
       w.k -= rad ? 1 : 0;
-      w.l -= rad ? 0 : dl;
-      w.s_rad = sh_sendx[w.k];
-      w.s_ax = (sh_planes[w.l + 1 - po] - z0) * tn;
+      w.l -= rad ? 0 : (UP ? 1 : -1);
+      w.load(TB[w.k]);
+      w.s_ax = (sh_planes[w.l + (UP ? 0 : 1)] - z0) * tn;
 #endif
     }
   }
@@ -355,6 +379,7 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<GP>& w, Physics<G, GP>&
 template <int GP>
 struct Replay {
   const Rec* rs;
+  const KSeg* TF;
   int q, qend, dq;  // next record to apply; stop index (exclusive)
   Rec cur;
   int cpc;
@@ -366,9 +391,9 @@ struct Replay {
     if (valid) {
       cur = rs[(size_t)q * kV2Threads];
       const int kk = cur.meta & 1023, l = (cur.meta >> 10) & 255;
-      const int2 ki = sh_kinfo[kk];
-      cpc = ki.y + l;
-      load_q<GP>(qt, (int64_t)(ki.x + l), cq);
+      const KSeg e = TF[kk];
+      cpc = e.ky + l;
+      load_q<GP>(qt, (int64_t)(e.kx + l), cq);
     }
   }
 };
@@ -390,11 +415,20 @@ __device__ __forceinline__ void replay_chunk(Replay<GP>& r, Physics<G, GP>& ph, 
   }
 }
 
+// one direction of one track through one chunk
+template <int G, int GP, bool UP>
+__device__ __forceinline__ void walk_chunk(int dir, WalkState<G, GP>& w, Physics<G, GP>& ph, const KSeg* TF,
+                                           const KSeg* TB, double z0, double tn, double isn, int c_lo, int c_hi) {
+  if (dir == 0) walk_fwd_chunk<G, GP, UP>(w, ph, TF, z0, tn, isn, c_hi);
+  else walk_bwd_chunk<G, GP, UP>(w, ph, TF, TB, z0, tn, isn, c_lo);
+}
+
 // HYBRID = false: pure on-the-fly sweep (the replay path is not compiled in, which keeps
 // the register budget for the walk); true: units may be EXP-preloaded.
 template <int G, int GP, bool HYBRID>
 __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a) {
-  extern __shared__ __align__(16) uint32_t tile[];
+  extern __shared__ __align__(16) uint8_t dsm[];
+  uint32_t* const tile = reinterpret_cast<uint32_t*>(dsm);
   __shared__ uint32_t s_unit;
   __shared__ int s_nchunk;
 
@@ -405,11 +439,13 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     sh_sig[q] = g < G ? c_sigt2[m * kMaxG + g] : 0.f;
   }
   for (int q = tid; q <= d.NL; q += blockDim.x) sh_planes[q] = d.planes[q];
-  // the tile starts zeroed; each flush re-zeroes exactly the cells it consumed
-  for (int q = tid; q < a.tile_words; q += blockDim.x) tile[q] = 0u;
+  // the tile starts zeroed; each flush re-zeroes exactly the cells it consumed, and
+  // bytes that held a unit's tables are re-zeroed before a later unit's tile uses them
+  for (int q = tid; q < a.dyn_bytes / 4; q += blockDim.x) tile[q] = 0u;
+  int clean_to = a.dyn_bytes;  // [0, clean_to) of the buffer is zero outside the live tile
   const float ps = (float)a.sc[SC_PSI_SCALE];
   constexpr int stride = GP + 1;
-  const int cap_cells = a.tile_words / stride;
+  const OtfView v{nullptr, nullptr, sh_planes, d.NL};
   double leak = 0.0;
   uint64_t nemit = 0;  // merged segment-direction emissions flushed by this thread
 
@@ -429,13 +465,21 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const double dz = d.an_dz[an], cot = d.an_cot[an];
     const double z0b = d.st_z0[s];
     const double zf = z0b + (double)U.i0 * dz, zl = z0b + (double)(U.i0 + U.n - 1) * dz;
-    const OtfView v{sh_sendx + 1, sh_reg, sh_planes, d.NL};
+    // per-unit tables at the top of the dynamic buffer, the tile below them
+    const int tab0 = (a.dyn_bytes - unit_table_bytes(nk)) & ~15;
+    KSeg* const TF = reinterpret_cast<KSeg*>(dsm + tab0);
+    KSeg* const TB = TF + nk;
+    int* const base = reinterpret_cast<int*>(TB + nk);
+    int* const chunk = base + nk + 1;
+    int cap_cells = tab0 / (4 * stride);
+    if (a.cap_cells > 0 && a.cap_cells < cap_cells) cap_cells = a.cap_cells;
+    for (int q = clean_to / 4 + tid; q < tab0 / 4; q += blockDim.x) tile[q] = 0u;
+    clean_to = tab0;
     // 1-2. stage the 2D segments, per-k layer windows of the band
     for (int kk = tid; kk < nk; kk += blockDim.x) {
       const double s1 = d.seg_send[sb + kk];
       const double s0 = kk ? d.seg_send[sb + kk - 1] : 0.0;
-      sh_sendx[kk + 1] = s1;
-      sh_reg[kk] = d.seg_region[sb + kk];
+      const int kx = (int)d.seg_region[sb + kk] * d.NL;
       double zlo = cot > 0 ? zf + s0 * cot : zf + s1 * cot;
       double zhi = cot > 0 ? zl + s1 * cot : zl + s0 * cot;
       zlo = zlo > 0.0 ? zlo : 0.0;
@@ -445,17 +489,17 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         lo = otf_layer_down(v, zlo);
         w = otf_layer_up(v, zhi) - lo + 1;
       }
-      sh_lo[kk] = lo;
-      sh_base[kk] = w;
+      TF[kk] = KSeg{s1, kx, lo};  // ky completed after the scan
+      TB[kk] = KSeg{s0, kx, lo};
+      base[kk] = w;
     }
     if (tid < kMaxG) sh_max[tid] = 0u;
-    if (tid == 0) sh_sendx[0] = 0.0;
     __syncthreads();
     if (warp == 0) {
       int carry = 0;
       for (int b0 = 0; b0 < nk; b0 += 32) {
         const int kk = b0 + lane;
-        const int w = kk < nk ? sh_base[kk] : 0;
+        const int w = kk < nk ? base[kk] : 0;
         int x = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -463,28 +507,30 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
           if (lane >= o) x += y;
         }
         if (kk < nk) {
-          const int base = carry + x - w;
-          sh_base[kk] = base;
-          sh_kinfo[kk] = make_int2((int)sh_reg[kk] * d.NL, base - sh_lo[kk]);
+          const int b = carry + x - w;
+          base[kk] = b;
+          const int ky = b - TF[kk].ky;
+          TF[kk].ky = ky;
+          TB[kk].ky = ky;
         }
         carry += __shfl_sync(0xffffffffu, x, 31);
       }
       if (lane == 0) {
-        sh_base[nk] = carry;
+        base[nk] = carry;
         // greedy chunks of consecutive k whose cells fit the tile
         int nc = 0, k0 = 0;
-        sh_chunk[0] = 0;
+        chunk[0] = 0;
         for (int kk = 0; kk < nk; ++kk) {
-          if (sh_base[kk + 1] - sh_base[k0] > cap_cells) {
+          if (base[kk + 1] - base[k0] > cap_cells) {
             if (kk == k0) {
               atomicAdd(a.err, 1);  // a single 2D segment's window exceeds the tile
               break;
             }
-            sh_chunk[++nc] = kk;
+            chunk[++nc] = kk;
             k0 = kk;
           }
         }
-        sh_chunk[++nc] = nk;
+        chunk[++nc] = nk;
         s_nchunk = nc;
       }
     }
@@ -517,7 +563,6 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const double tn = d.an_tan[an], isn = d.an_invsin[an], Lt = d.t_len[t];
     const double z0 = z0b + (double)(U.i0 + p) * dz;
     const bool up = cot > 0;
-    const int dl = up ? 1 : -1, po = up ? 1 : 0;
     const float cw = d.an_c[an];
     const bool otf = !HYBRID || exp_off == kNoExp;
     double s_in = 0, s_out = 0;
@@ -538,7 +583,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
 #pragma unroll
       for (int g = 0; g < G; ++g)
         ph.psi[g] = active ? a.psi_in[(size_t)(2 * id + dir) * GP + g] * ps * ph.scl[g] : 0.f;
-      WalkState<GP> w;
+      WalkState<G, GP> w;
       Replay<GP> r;
       if (otf) {
         w.done = !active;
@@ -552,29 +597,32 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
           w.s_end = s_out;
           if (s_in > 0.0) {
             w.l = up ? 0 : d.NL - 1;
-            w.k = (int)otf_seg_after(v, 0, nk, s_in);
+            w.k = kseg_after(TF, nk, s_in);
           } else {
             w.l = up ? otf_layer_up(v, z0) : otf_layer_down(v, z0);
             w.k = 0;
           }
+          w.load(TF[w.k]);
+          w.s_ax = (sh_planes[up ? w.l + 1 : w.l] - z0) * tn;
         } else {
           w.s = s_out;
           w.s_end = s_in;
           if (s_out < Lt) {
             w.l = up ? d.NL - 1 : 0;
-            w.k = (int)otf_seg_upto(v, 0, nk, s_out);
+            w.k = kseg_upto(TF, nk, s_out);
           } else {
             const double z_out = z0 + Lt * cot;
             w.l = up ? otf_layer_down(v, z_out) : otf_layer_up(v, z_out);
             w.k = nk - 1;
           }
+          w.load(TB[w.k]);
+          w.s_ax = (sh_planes[up ? w.l : w.l + 1] - z0) * tn;
         }
-        w.s_rad = active ? sh_sendx[dir == 0 ? w.k + 1 : w.k] : 0.0;
-        w.s_ax = active ? (sh_planes[dir == 0 ? w.l + po : w.l + 1 - po] - z0) * tn : 0.0;
       } else {
         // EXP: this thread's preloaded records, first to last or last to first
         const int nrec = active ? (int)a.cost[id] : 0;
         r.rs = a.store + exp_off + tid;
+        r.TF = TF;
         r.q = dir == 0 ? 0 : nrec - 1;
         r.qend = dir == 0 ? nrec : -1;
         r.dq = dir == 0 ? 1 : -1;
@@ -583,23 +631,24 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
 #pragma unroll 1
       for (int ci = 0; ci < nchunk; ++ci) {
         const int c = dir == 0 ? ci : nchunk - 1 - ci;
-        const int k_lo = sh_chunk[c], k_hi = sh_chunk[c + 1];
-        const int cb = sh_base[k_lo];
+        const int k_lo = chunk[c], k_hi = chunk[c + 1];
+        const int cb = base[k_lo], ce = base[k_hi];
         ph.ctile = tile - cb * stride;
 #ifdef MOC_DEBUG_WALK
         ph.dbg_lo = cb;
-        ph.dbg_hi = sh_base[k_hi];
+        ph.dbg_hi = ce;
         ph.dbg_dir = dir;
 #endif
         if (!otf) replay_chunk(r, ph, k_lo, k_hi);
-        else if (dir == 0) walk_fwd_chunk(w, ph, z0, tn, isn, dl, po, sh_base[k_hi]);
-        else walk_bwd_chunk(w, ph, z0, tn, isn, dl, po, cb);
+        else if (up) walk_chunk<G, GP, true>(dir, w, ph, TF, TB, z0, tn, isn, cb, ce);
+        else walk_chunk<G, GP, false>(dir, w, ph, TF, TB, z0, tn, isn, cb, ce);
         __syncthreads();
         // 4. flush the chunk: c_{a,n} * fixed-point sums -> global tally (fp32 vector
         //    reductions), re-zeroing every consumed cell for the next chunk
         for (int kk = k_lo + warp; kk < k_hi; kk += nw) {
-          const int b = sh_base[kk] - cb, wd = sh_base[kk + 1] - sh_base[kk];
-          const int64_t jr = (int64_t)sh_reg[kk] * d.NL + sh_lo[kk];
+          const int bk = base[kk], b = bk - cb, wd = base[kk + 1] - bk;
+          const KSeg e = TF[kk];
+          const int64_t jr = (int64_t)e.kx + (bk - e.ky);  // FSR of the window's first layer
           for (int x = lane; x < wd; x += 32) {
             uint32_t* cell = tile + (b + x) * stride;
             const uint32_t cnt = cell[GP];
