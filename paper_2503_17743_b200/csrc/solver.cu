@@ -507,7 +507,7 @@ struct moc_solver {
   uint32_t* d_counter = nullptr;
   float *d_rmax = nullptr, *d_qmax_t = nullptr, *d_tally32 = nullptr;
   int* d_err = nullptr;
-  int cap_cells = 0;  // forced tile cap in cells (moc_solver_opts.tile_cells), 0 = none
+  int cap_cells = 0;  // v2 tile capacity in cells (sweep_v2.cuh layout)
   int lane_lg = -1;  // forced log2 v2 lane stride (MOC_V2_LANE_STRIDE), -1 = per unit
   double h_lane = 0;     // thinnest axial layer / 3 (sweep_v2.cuh lane_lg_of)
   size_t v2_smem = 0;
@@ -960,11 +960,13 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       if (g.NL + 1 > kMaxPlanes) throw Error(MOC_E_CAPACITY, "more than 255 axial layers");
       v2_configure_any(s);  // dynamic shared memory from the kernel's static footprint
       // the tile left below the largest unit's tables must hold two full layer columns
-      if (((int64_t)s->v2_smem - unit_table_bytes((int)max_nk)) / (4 * (s->GP + 1)) < 2 * g.NL)
-        throw Error(MOC_E_CAPACITY, "axial mesh too fine for the tally tile");
+      s->cap_cells = (int)std::min<int64_t>(
+          cap_max_cells(s->GP),
+          (((int64_t)s->v2_smem - unit_table_bytes((int)max_nk) - tile_words_offset(s->GP)) / (4 * (s->GP + 1))) & ~7);
+      if (s->cap_cells < 2 * g.NL) throw Error(MOC_E_CAPACITY, "axial mesh too fine for the tally tile");
       if (s->opts.tile_cells > 0) {
         if (s->opts.tile_cells < g.NL) throw Error(MOC_E_PARAM, "tile_cells must be >= the number of axial layers");
-        s->cap_cells = s->opts.tile_cells;
+        s->cap_cells = std::min(s->cap_cells, (s->opts.tile_cells + 7) & ~7);
       }
       {
         double hmin = 1e300;

@@ -60,9 +60,15 @@ struct __align__(16) KSeg {
   int ky;  // first tile cell of k - lo_k: cell = ky + layer
 };
 
-// Dynamic shared memory of one CTA: [tile cells ... | TF[nk] | TB[nk] | base[nk+1] |
-// chunk[nk+1]]; the tables are sized per unit from the top, the tile takes the rest.
+// Dynamic shared memory of one CTA, bottom up: cell -> 2D segment k [kCapMax] u16, the
+// tile [cap][GP + 1] u32 (GP group words + the segment count; the odd stride keeps lanes
+// in different cells on different banks; compile-time offset, so an emit address is one
+// register plus a constant base), and from the top the per-unit tables (TF[nk] | TB[nk]
+// | base[nk+1] | chunk[nk+1]).  cap <= kCapMax is fixed per solver (largest nk), so the
+// tile never moves and stays zero between flushes.
 __host__ __device__ constexpr int unit_table_bytes(int nk) { return 32 * nk + ((8 * (nk + 1) + 15) & ~15); }
+__host__ __device__ constexpr int cap_max_cells(int GP) { return (48000 / (4 * GP + 6)) & ~7; }
+__host__ __device__ constexpr int tile_words_offset(int GP) { return 2 * cap_max_cells(GP); }  // bytes
 
 struct Unit {
   uint32_t stack, i0, n, cost;
@@ -94,7 +100,7 @@ struct V2Args {
   const Rec* store;     // EXP record store
   const uint32_t* cost; // exact merged segments per track (EXP replay length)
   int dyn_bytes;        // dynamic shared memory per CTA
-  int cap_cells;        // tile cap in cells (tests force many chunks), <= 0: none
+  int cap_cells;        // tile capacity in cells (multiple of 8)
   double h_lane;        // thinnest axial layer / 3 (lane_lg_of)
   int lane_lg;          // forced log2 lane stride, -1 = per unit (lane_lg_of)
   int* err;
@@ -180,7 +186,7 @@ struct Physics {
   float scl[G];
   const uint8_t* mat;
   const float* qt;
-  uint32_t* ctile;  // tile - (first cell of the current chunk) * (GP + 1)
+  int cb;  // first cell of the current chunk (tile cell 0)
 #ifdef MOC_DEBUG_WALK
   int dbg_lo, dbg_hi, dbg_dir;
 #endif
@@ -193,7 +199,9 @@ struct Physics {
       return;
     }
 #endif
-    uint32_t* cell = ctile + pc * (GP + 1);
+    extern __shared__ __align__(16) uint8_t dsm[];
+    const int x = pc - cb;
+    uint32_t* cell = reinterpret_cast<uint32_t*>(dsm + tile_words_offset(GP)) + x * (GP + 1);
     atomicAdd(cell + GP, 1u);
     float sg[GP];
     if constexpr (GP % 4 == 0) {
@@ -428,7 +436,9 @@ __device__ __forceinline__ void walk_chunk(int dir, WalkState<G, GP>& w, Physics
 template <int G, int GP, bool HYBRID>
 __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a) {
   extern __shared__ __align__(16) uint8_t dsm[];
-  uint32_t* const tile = reinterpret_cast<uint32_t*>(dsm);
+  const int cap = a.cap_cells;
+  uint16_t* const cellk = reinterpret_cast<uint16_t*>(dsm);                         // [kCapMax]
+  uint32_t* const cells = reinterpret_cast<uint32_t*>(dsm + tile_words_offset(GP));  // [cap][GP + 1]
   __shared__ uint32_t s_unit;
   __shared__ int s_nchunk;
 
@@ -439,12 +449,9 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     sh_sig[q] = g < G ? c_sigt2[m * kMaxG + g] : 0.f;
   }
   for (int q = tid; q <= d.NL; q += blockDim.x) sh_planes[q] = d.planes[q];
-  // the tile starts zeroed; each flush re-zeroes exactly the cells it consumed, and
-  // bytes that held a unit's tables are re-zeroed before a later unit's tile uses them
-  for (int q = tid; q < a.dyn_bytes / 4; q += blockDim.x) tile[q] = 0u;
-  int clean_to = a.dyn_bytes;  // [0, clean_to) of the buffer is zero outside the live tile
+  // the tile starts zeroed; each flush re-zeroes exactly the cells it consumed
+  for (int q = tid; q < cap * (GP + 1); q += blockDim.x) cells[q] = 0u;
   const float ps = (float)a.sc[SC_PSI_SCALE];
-  constexpr int stride = GP + 1;
   const OtfView v{nullptr, nullptr, sh_planes, d.NL};
   double leak = 0.0;
   uint64_t nemit = 0;  // merged segment-direction emissions flushed by this thread
@@ -471,10 +478,6 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     KSeg* const TB = TF + nk;
     int* const base = reinterpret_cast<int*>(TB + nk);
     int* const chunk = base + nk + 1;
-    int cap_cells = tab0 / (4 * stride);
-    if (a.cap_cells > 0 && a.cap_cells < cap_cells) cap_cells = a.cap_cells;
-    for (int q = clean_to / 4 + tid; q < tab0 / 4; q += blockDim.x) tile[q] = 0u;
-    clean_to = tab0;
     // 1-2. stage the 2D segments, per-k layer windows of the band
     for (int kk = tid; kk < nk; kk += blockDim.x) {
       const double s1 = d.seg_send[sb + kk];
@@ -521,7 +524,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         int nc = 0, k0 = 0;
         chunk[0] = 0;
         for (int kk = 0; kk < nk; ++kk) {
-          if (base[kk + 1] - base[k0] > cap_cells) {
+          if (base[kk + 1] - base[k0] > cap) {
             if (kk == k0) {
               atomicAdd(a.err, 1);  // a single 2D segment's window exceeds the tile
               break;
@@ -633,7 +636,12 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const int c = dir == 0 ? ci : nchunk - 1 - ci;
         const int k_lo = chunk[c], k_hi = chunk[c + 1];
         const int cb = base[k_lo], ce = base[k_hi];
-        ph.ctile = tile - cb * stride;
+        ph.cb = cb;
+        // cell -> k map of the chunk for the flush (the previous flush ended at a barrier)
+        for (int kk = k_lo + warp; kk < k_hi; kk += nw) {
+          const int b = base[kk] - cb, wd = base[kk + 1] - base[kk];
+          for (int x = lane; x < wd; x += 32) cellk[b + x] = (uint16_t)kk;
+        }
 #ifdef MOC_DEBUG_WALK
         ph.dbg_lo = cb;
         ph.dbg_hi = ce;
@@ -643,33 +651,33 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         else if (up) walk_chunk<G, GP, true>(dir, w, ph, TF, TB, z0, tn, isn, cb, ce);
         else walk_chunk<G, GP, false>(dir, w, ph, TF, TB, z0, tn, isn, cb, ce);
         __syncthreads();
-        // 4. flush the chunk: c_{a,n} * fixed-point sums -> global tally (fp32 vector
-        //    reductions), re-zeroing every consumed cell for the next chunk
-        for (int kk = k_lo + warp; kk < k_hi; kk += nw) {
-          const int bk = base[kk], b = bk - cb, wd = base[kk + 1] - bk;
-          const KSeg e = TF[kk];
-          const int64_t jr = (int64_t)e.kx + (bk - e.ky);  // FSR of the window's first layer
-          for (int x = lane; x < wd; x += 32) {
-            uint32_t* cell = tile + (b + x) * stride;
-            const uint32_t cnt = cell[GP];
-            if (!cnt) continue;
-            nemit += cnt;
-            float val[GP];
+        // 4. flush the chunk, one cell per thread: c_{a,n} * fixed-point sums -> global
+        //    tally (fp32 vector reductions), re-zeroing every consumed cell
+        for (int x = tid; x < ce - cb; x += blockDim.x) {
+          uint32_t* cp = cells + (size_t)x * (GP + 1);
+          const uint32_t cnt = cp[GP];
+          if (!cnt) continue;
+          cp[GP] = 0u;
+          nemit += cnt;
+          const KSeg e = TF[cellk[x]];
+          const int64_t j = (int64_t)(e.kx - e.ky) + cb + x;  // FSR of cell cb + x = ky + layer
+          uint32_t raw[GP];
 #pragma unroll
-            for (int g = 0; g < GP; ++g) {
-              val[g] = g < G ? (float)(int)(cell[g] - cnt * kMagicBits) * (sh_iscale[g] * cw) : 0.f;
-              cell[g] = 0u;
-            }
-            cell[GP] = 0u;
-            float* dst = a.tally + (jr + x) * GP;
-            if constexpr (GP % 4 == 0) {
+          for (int g = 0; g < GP; ++g) {
+            raw[g] = cp[g];
+            cp[g] = 0u;
+          }
+          float val[GP];
 #pragma unroll
-              for (int h = 0; h < GP / 4; ++h)
-                red_add_v4(dst + 4 * h, val[4 * h], val[4 * h + 1], val[4 * h + 2], val[4 * h + 3]);
-            } else {
+          for (int g = 0; g < GP; ++g) val[g] = g < G ? (float)(int)(raw[g] - cnt * kMagicBits) * (sh_iscale[g] * cw) : 0.f;
+          float* dst = a.tally + j * GP;
+          if constexpr (GP % 4 == 0) {
 #pragma unroll
-              for (int g = 0; g < G; ++g) atomicAdd(dst + g, val[g]);
-            }
+            for (int h = 0; h < GP / 4; ++h)
+              red_add_v4(dst + 4 * h, val[4 * h], val[4 * h + 1], val[4 * h + 2], val[4 * h + 3]);
+          } else {
+#pragma unroll
+            for (int g = 0; g < G; ++g) atomicAdd(dst + g, val[g]);
           }
         }
         __syncthreads();
