@@ -498,6 +498,17 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     }
     if (tid < kMaxG) sh_max[tid] = 0u;
     __syncthreads();
+    // 3. one track per thread (member_of: neighbouring members share a warp); its incoming
+    //    psi loads are issued here so their HBM latency overlaps the scan below
+    const int p = member_of(tid, lane_lg_of(dz, a.h_lane, a.lane_lg, (int)U.n));
+    const bool active = p < (int)U.n;
+    const uint32_t id = d.st_first[s] + U.i0 + (uint32_t)p;
+    float fpsi[G], bpsi[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      fpsi[g] = active ? a.psi_in[(size_t)(2 * id) * GP + g] : 0.f;
+      bpsi[g] = active ? a.psi_in[(size_t)(2 * id + 1) * GP + g] : 0.f;
+    }
     if (warp == 0) {
       int carry = 0;
       for (int b0 = 0; b0 < nk; b0 += 32) {
@@ -518,35 +529,39 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         }
         carry += __shfl_sync(0xffffffffu, x, 31);
       }
-      if (lane == 0) {
-        base[nk] = carry;
-        // greedy chunks of consecutive k whose cells fit the tile
-        int nc = 0, k0 = 0;
-        chunk[0] = 0;
-        for (int kk = 0; kk < nk; ++kk) {
-          if (base[kk + 1] - base[k0] > cap) {
-            if (kk == k0) {
-              atomicAdd(a.err, 1);  // a single 2D segment's window exceeds the tile
-              break;
-            }
-            chunk[++nc] = kk;
-            k0 = kk;
+      if (lane == 0) base[nk] = carry;
+      __syncwarp();
+      // greedy chunks of consecutive k whose cells fit the tile: chunk [k0, k1) ends at
+      // the first k1 with base[k1 + 1] - base[k0] > cap, found 32 k at a time by ballot
+      int nc = 0, k0 = 0;
+      while (k0 < nk) {
+        const int b0 = base[k0];
+        int k1 = nk;
+        for (int kb = k0; kb < nk; kb += 32) {
+          const int kk = kb + lane;
+          const unsigned over = __ballot_sync(0xffffffffu, kk < nk && base[kk + 1] - b0 > cap);
+          if (over) {
+            k1 = kb + __ffs(over) - 1;
+            break;
           }
         }
-        chunk[++nc] = nk;
+        if (k1 == k0) {  // a single 2D segment's window exceeds the tile
+          if (lane == 0) atomicAdd(a.err, 1);
+          k1 = nk;
+        }
+        if (lane == 0) chunk[nc] = k0;
+        ++nc;
+        k0 = k1;
+      }
+      if (lane == 0) {
+        chunk[nc] = nk;
         s_nchunk = nc;
       }
     }
-    // 3. one track per thread (member_of: neighbouring members share a warp)
-    const int p = member_of(tid, lane_lg_of(dz, a.h_lane, a.lane_lg, (int)U.n));
-    const bool active = p < (int)U.n;
-    const uint32_t id = d.st_first[s] + U.i0 + (uint32_t)p;
     Physics<G, GP> ph;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const float f = active ? a.psi_in[(size_t)(2 * id) * GP + g] * ps : 0.f;
-      const float b = active ? a.psi_in[(size_t)(2 * id + 1) * GP + g] * ps : 0.f;
-      float m = fmaxf(f, b);
+      float m = fmaxf(fpsi[g], bpsi[g]) * ps;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
       if (lane == 0) atomicMax(&sh_max[g], __float_as_uint(m));
