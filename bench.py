@@ -244,7 +244,11 @@ def run_ours(args):
     peaks, kind = _peaks()
     mhz_max = float(peaks.get("sm_max_mhz", 1965.0))
     sweep_med = float(np.median(sweep_ms))
-    achieved = nint / (sweep_med * 1e-3)
+    # the roofline is per GPU: this rank's integrations (its emitted segment-directions x G,
+    # = nint on one GPU) over its own sweep time
+    emitted = s.timings().get("emitted_last", -1)
+    nint_rank = emitted * G if emitted and emitted > 0 else nint / world
+    achieved = nint_rank / (sweep_med * 1e-3)
     peak = r_alu(G, mhz_max)
     kerr = k_eff_errors(M, dev) if rank == 0 and not args.no_parity else None
     cpu = None

@@ -387,18 +387,18 @@ class Solver:
             host = dist.get_backend() != "nccl"  # gloo (tests): stage through host memory
             for _ in range(int(n)):
                 self._call(lib().moc_iteration_sweep)
+                # both collectives are called on every rank every iteration (a rank with an
+                # empty halo still takes part, or the others would wait forever)
                 if host:
                     t = c["tally"].cpu()
                     dist.all_reduce(t)
                     c["tally"].copy_(t)
-                    if c["send"].numel() or c["recv"].numel():
-                        rbuf = c["recv"].cpu()
-                        dist.all_to_all_single(rbuf, c["send"].cpu(), c["recv_splits"], c["send_splits"])
-                        c["recv"].copy_(rbuf)
+                    rbuf = c["recv"].cpu()
+                    dist.all_to_all_single(rbuf, c["send"].cpu(), c["recv_splits"], c["send_splits"])
+                    c["recv"].copy_(rbuf)
                 else:
                     dist.all_reduce(c["tally"])
-                    if c["send"].numel() or c["recv"].numel():
-                        dist.all_to_all_single(c["recv"], c["send"], c["recv_splits"], c["send_splits"])
+                    dist.all_to_all_single(c["recv"], c["send"], c["recv_splits"], c["send_splits"])
                 self._call(lib().moc_iteration_finish)
             n = 0
         self._call(lib().moc_iterate, int(n), C.byref(k), C.byref(r))
