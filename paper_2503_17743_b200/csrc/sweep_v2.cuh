@@ -43,6 +43,9 @@ constexpr uint32_t kMagicBits = 0x4B400000u;  // bits of 1.5 * 2^23
 constexpr float kMagic = 12582912.0f;         // 1.5 * 2^23
 constexpr float kFixOne = 2097152.0f;         // 2^21: max |term| in fixed point
 constexpr uint64_t kNoExp = ~0ull;            // unit not preloaded (on-the-fly)
+// epsilon_L in the constant bank: DSETP reads it as an operand, where the immediate form
+// would cost two uniform moves per raw piece (same value as otf.h kEpsL)
+__constant__ double c_epsL = kEpsL;
 
 // per-kernel shared tables; the per-unit tables share the dynamic buffer with the tile
 __shared__ double sh_planes[kMaxPlanes];  // axial planes
@@ -286,7 +289,7 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
     sn = last ? w.s_end : sn;
     const double L3d = (sn - w.s) * isn;
     const float L3 = (float)L3d;
-    if (L3d < kEpsL) {
+    if (L3d < c_epsL) {
       if (w.pc >= 0) {
         w.pL += L3;  // a sliver merges into the segment before it
       } else {
@@ -350,7 +353,7 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, G
     sp = last ? w.s_end : sp;
     const double L3d = (w.s - sp) * isn;
     const float L3 = (float)L3d;
-    if (L3d < kEpsL) {
+    if (L3d < c_epsL) {
       w.carry += L3;
       if (w.pc < 0) w.fkl = w.k | (w.l << 16);  // the forward-first sliver wins
     } else {
