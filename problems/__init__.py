@@ -126,6 +126,33 @@ def xs_c5g7_synthetic(seed: int = SEED):
 # ----------------------------------------------------------------------------
 # geometry helpers
 # ----------------------------------------------------------------------------
+def xs_synthetic(G: int, n_mat: int = 7, seed: int = SEED):
+    """G-group synthetic set with ``n_mat`` materials (tests of other group counts):
+    material 0 and 1 fissile (fuel-like), the rest moderator / absorber-like.
+    Sigma_t in [0.2, 2.5], scattering ratio 0.5-0.95 (fuel) / 0.85-0.99 (others),
+    downscatter to up to 2 groups below plus within-group, chi on the fastest
+    groups; deterministic in ``seed``."""
+    rng = np.random.Generator(np.random.PCG64(seed + 1000 * G + n_mat))
+    chi = np.zeros(G)
+    chi[: max(1, (G + 1) // 2)] = rng.uniform(0.2, 1.0, max(1, (G + 1) // 2))
+    chi /= chi.sum()
+    mats = []
+    for m in range(n_mat):
+        fis = m < 2
+        st = rng.uniform(0.2, 2.5, G)
+        ratio = rng.uniform(0.5, 0.95, G) if fis else rng.uniform(0.85, 0.99, G)
+        ss = np.zeros((G, G))
+        for g in range(G):
+            tg = list(range(g, min(G, g + 3)))
+            w = rng.uniform(0.2, 1.0, len(tg))
+            w[0] *= 3.0
+            ss[g, tg] = ratio[g] * st[g] * w / w.sum()
+        nf = rng.uniform(0.01, 0.3, G) * st if fis else np.zeros(G)
+        mats.append(dict(name=f"syn{G}g{m}", sigma_t=st.tolist(), sigma_s=ss.tolist(), nu_sigma_f=nf.tolist(),
+                         chi=(chi if fis else np.zeros(G)).tolist()))
+    return mats
+
+
 def _uniform_planes(n, h):
     return [round(i * h, 12) for i in range(n + 1)]
 

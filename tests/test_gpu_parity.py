@@ -70,6 +70,21 @@ def test_fixed_iteration_parity_small_lattice(M, oracle_mod, schedule):
     np.testing.assert_allclose(kh, ref["k_hist"], atol=1e-5)
 
 
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 5, 8])
+def test_other_group_counts_parity(M, oracle_mod, G):
+    """Every group-count instantiation of the sweep (G = 1, 2, 3 -> 4, 4, 5 -> 8 padded,
+    and G = 8 where the source has no pad slot and the material comes from mat[]):
+    fixed-iteration parity against the oracle on a small heterogeneous lattice."""
+    prob = P.small_lattice(3, 3, 4, xs=P.xs_synthetic(G))
+    s = M.Solver(M.Problem(prob))
+    k, _ = s.iterate(6)
+    _check_emitted(s)
+    ref = oracle_mod.Oracle(prob).solve(fixed_iters=6)
+    assert k == pytest.approx(ref["k"], abs=1e-5)
+    linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
+    assert linf < 1e-4, (linf, rel)
+
+
 @pytest.mark.parametrize("tile_cells", [4, 9, 37])
 def test_many_chunk_tiles_parity(M, oracle_mod, tile_cells):
     """Force tiny shared-memory tally chunks so every work unit is walked in many

@@ -306,6 +306,17 @@ def test_k_inf_multigroup(oracle_mod, variant):
         assert kd == pytest.approx(GOLD["k_inf_2g_fuel"]["k"], abs=1e-12)
 
 
+@pytest.mark.parametrize("G", [3, 8])
+def test_k_inf_other_group_counts(oracle_mod, G):
+    """SURVEY P12 for the other group counts the GPU instantiates (G = 3 pads to 4, G = 8
+    has no pad slot): homogeneous reflective cube of a synthetic fissile material."""
+    m = P.xs_synthetic(G)[0]
+    prob = P.homogeneous_cube(side=2.0, ncell=1, nlayers=2, xs=[m])
+    o = oracle_mod.Oracle(prob)
+    r = o.solve(max_iter=4000, tol_k=1e-12, tol_src=1e-11)
+    assert r["k"] == pytest.approx(_kinf_dense(m), abs=1e-9)
+
+
 def _slab_1d(prob, pol):
     """Independent 1D step-characteristics power iteration (test's own) with the
     oracle's corrected polar cosines and weights: directions +-mu_{a,n} for
