@@ -63,15 +63,14 @@ struct __align__(16) KSeg {
   int ky;  // first tile cell of k - lo_k: cell = ky + layer
 };
 
-// Dynamic shared memory of one CTA, bottom up: cell -> 2D segment k [kCapMax] u16, the
-// tile [cap][GP + 1] u32 (GP group words + the segment count; the odd stride keeps lanes
-// in different cells on different banks; compile-time offset, so an emit address is one
-// register plus a constant base), and from the top the per-unit tables (TF[nk] | TB[nk]
-// | base[nk+1] | chunk[nk+1]).  cap <= kCapMax is fixed per solver (largest nk), so the
-// tile never moves and stays zero between flushes.
+// Dynamic shared memory of one CTA: the tile [cap][GP + 1] u32 from the bottom (GP group
+// words + the segment count; the odd stride keeps lanes in different cells on different
+// banks), and from the top the per-unit tables (TF[nk] | TB[nk] | base[nk+1] |
+// chunk[nk+1]).  cap <= kCapMax is fixed per solver (largest nk), so the tile never moves
+// and stays zero between flushes.
 __host__ __device__ constexpr int unit_table_bytes(int nk) { return 32 * nk + ((8 * (nk + 1) + 15) & ~15); }
-__host__ __device__ constexpr int cap_max_cells(int GP) { return (48000 / (4 * GP + 6)) & ~7; }
-__host__ __device__ constexpr int tile_words_offset(int GP) { return 2 * cap_max_cells(GP); }  // bytes
+__host__ __device__ constexpr int cap_max_cells(int GP) { return (56000 / (4 * GP + 4)) & ~7; }
+__host__ __device__ constexpr int tile_words_offset(int GP) { return 0 * GP; }  // bytes
 
 struct Unit {
   uint32_t stack, i0, n, cost;
@@ -434,13 +433,22 @@ __device__ __forceinline__ void walk_chunk(int dir, WalkState<G, GP>& w, Physics
   else walk_bwd_chunk<G, GP, UP>(w, ph, TF, TB, z0, tn, isn, c_lo);
 }
 
+// largest k in [k_lo, k_hi) with base[k] <= c (the 2D segment owning tile cell c)
+__device__ __forceinline__ int k_of_cell(const int* base, int k_lo, int k_hi, int c) {
+  int lo = k_lo, hi = k_hi - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (base[mid] <= c) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 // HYBRID = false: pure on-the-fly sweep (the replay path is not compiled in, which keeps
 // the register budget for the walk); true: units may be EXP-preloaded.
 template <int G, int GP, bool HYBRID>
 __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a) {
   extern __shared__ __align__(16) uint8_t dsm[];
   const int cap = a.cap_cells;
-  uint16_t* const cellk = reinterpret_cast<uint16_t*>(dsm);                         // [kCapMax]
   uint32_t* const cells = reinterpret_cast<uint32_t*>(dsm + tile_words_offset(GP));  // [cap][GP + 1]
   __shared__ uint32_t s_unit;
   __shared__ int s_nchunk;
@@ -655,11 +663,6 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const int k_lo = chunk[c], k_hi = chunk[c + 1];
         const int cb = base[k_lo], ce = base[k_hi];
         ph.cb = cb;
-        // cell -> k map of the chunk for the flush (the previous flush ended at a barrier)
-        for (int kk = k_lo + warp; kk < k_hi; kk += nw) {
-          const int b = base[kk] - cb, wd = base[kk + 1] - base[kk];
-          for (int x = lane; x < wd; x += 32) cellk[b + x] = (uint16_t)kk;
-        }
 #ifdef MOC_DEBUG_WALK
         ph.dbg_lo = cb;
         ph.dbg_hi = ce;
@@ -669,15 +672,22 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         else if (up) walk_chunk<G, GP, true>(dir, w, ph, TF, TB, z0, tn, isn, cb, ce);
         else walk_chunk<G, GP, false>(dir, w, ph, TF, TB, z0, tn, isn, cb, ce);
         __syncthreads();
-        // 4. flush the chunk, one cell per thread: c_{a,n} * fixed-point sums -> global
-        //    tally (fp32 vector reductions), re-zeroing every consumed cell
-        for (int x = tid; x < ce - cb; x += blockDim.x) {
+        // 4. flush the chunk: c_{a,n} * fixed-point sums -> global tally (fp32 vector
+        //    reductions), re-zeroing every consumed cell.  Each warp takes a contiguous
+        //    eighth of the chunk's cells, lane-strided, so a lane's 2D segment k (for the
+        //    cell's FSR) advances by a step or two per cell from one binary search.
+        const int per = (ce - cb + nw - 1) / nw;
+        const int x1 = min(ce - cb, (warp + 1) * per);
+        int kc = -1;
+        for (int x = warp * per + lane; x < x1; x += 32) {
           uint32_t* cp = cells + (size_t)x * (GP + 1);
           const uint32_t cnt = cp[GP];
           if (!cnt) continue;
           cp[GP] = 0u;
           nemit += cnt;
-          const KSeg e = TF[cellk[x]];
+          if (kc < 0) kc = k_of_cell(base, k_lo, k_hi, cb + x);
+          while (base[kc + 1] <= cb + x) ++kc;
+          const KSeg e = TF[kc];
           const int64_t j = (int64_t)(e.kx - e.ky) + cb + x;  // FSR of cell cb + x = ky + layer
           uint32_t raw[GP];
 #pragma unroll
