@@ -508,6 +508,7 @@ struct moc_solver {
   float *d_rmax = nullptr, *d_qmax_t = nullptr, *d_tally32 = nullptr;
   int* d_err = nullptr;
   int cap_cells = 0;  // v2 tile capacity in cells (sweep_v2.cuh layout)
+  int tile_off = 0;   // v2 tile byte offset (above the largest unit's tables)
   int lane_lg = -1;  // forced log2 v2 lane stride (MOC_V2_LANE_STRIDE), -1 = per unit
   double h_lane = 0;     // thinnest axial layer / 3 (sweep_v2.cuh lane_lg_of)
   size_t v2_smem = 0;
@@ -580,7 +581,7 @@ void run_sweep(moc_solver* s) {
     a.psi_out = s->d_psi[out];
     a.tally = s->d_tally32;
     a.sc = s->d_sc;
-    a.dyn_bytes = (int)s->v2_smem;
+    a.tile_off = s->tile_off;
     a.cap_cells = s->cap_cells;
     a.lane_lg = s->lane_lg;
     a.h_lane = s->h_lane;
@@ -962,7 +963,8 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       // the tile left below the largest unit's tables must hold two full layer columns
       s->cap_cells = (int)std::min<int64_t>(
           cap_max_cells(s->GP),
-          (((int64_t)s->v2_smem - unit_table_bytes((int)max_nk) - tile_words_offset(s->GP)) / (4 * (s->GP + 1))) & ~7);
+          (((int64_t)s->v2_smem - unit_table_bytes((int)max_nk)) / (4 * (s->GP + 1))) & ~7);
+      s->tile_off = (unit_table_bytes((int)max_nk) + 15) & ~15;
       if (s->cap_cells < 2 * g.NL) throw Error(MOC_E_CAPACITY, "axial mesh too fine for the tally tile");
       if (s->opts.tile_cells > 0) {
         if (s->opts.tile_cells < g.NL) throw Error(MOC_E_PARAM, "tile_cells must be >= the number of axial layers");

@@ -35,7 +35,10 @@ namespace {
 #ifndef MOC_V2_CTAS_PER_SM
 #define MOC_V2_CTAS_PER_SM 4
 #endif
-constexpr int kV2Threads = 256;
+#ifndef MOC_V2_THREADS
+#define MOC_V2_THREADS 256
+#endif
+constexpr int kV2Threads = MOC_V2_THREADS;  // one stack band of up to this many members per CTA
 constexpr int kV2MinBlocks = MOC_V2_CTAS_PER_SM;  // CTAs per SM the register/smem budget targets
 constexpr int kMaxK = 512;                    // max 2D segments per 2D track (host-checked)
 constexpr int kMaxPlanes = 256;               // axial planes staged in shared memory (host-checked)
@@ -63,14 +66,14 @@ struct __align__(16) KSeg {
   int ky;  // first tile cell of k - lo_k: cell = ky + layer
 };
 
-// Dynamic shared memory of one CTA: the tile [cap][GP + 1] u32 from the bottom (GP group
-// words + the segment count; the odd stride keeps lanes in different cells on different
-// banks), and from the top the per-unit tables (TF[nk] | TB[nk] | base[nk+1] |
-// chunk[nk+1]).  cap <= kCapMax is fixed per solver (largest nk), so the tile never moves
-// and stays zero between flushes.
+// Dynamic shared memory of one CTA: the per-unit tables from the bottom (TF[nk] at offset
+// 0, so a radial step's address is one shift from the buffer base | TB[nk] | base[nk+1] |
+// chunk[nk+1]), then the tile [cap][GP + 1] u32 at a per-solver offset (tile_off >= the
+// largest unit's tables; GP group words + the segment count, the odd stride keeping lanes
+// in different cells on different banks).  The tile never moves and stays zero between
+// flushes.
 __host__ __device__ constexpr int unit_table_bytes(int nk) { return 32 * nk + ((8 * (nk + 1) + 15) & ~15); }
 __host__ __device__ constexpr int cap_max_cells(int GP) { return (56000 / (4 * GP + 4)) & ~7; }
-__host__ __device__ constexpr int tile_words_offset(int GP) { return 0 * GP; }  // bytes
 
 struct Unit {
   uint32_t stack, i0, n, cost;
@@ -101,7 +104,7 @@ struct V2Args {
   double* sc;
   const Rec* store;     // EXP record store
   const uint32_t* cost; // exact merged segments per track (EXP replay length)
-  int dyn_bytes;        // dynamic shared memory per CTA
+  int tile_off;         // byte offset of the tile in the dynamic buffer (multiple of 16)
   int cap_cells;        // tile capacity in cells (multiple of 8)
   double h_lane;        // thinnest axial layer / 3 (lane_lg_of)
   int lane_lg;          // forced log2 lane stride, -1 = per unit (lane_lg_of)
@@ -120,7 +123,8 @@ struct V2Args {
 __device__ __forceinline__ int lane_lg_of(double dz, double h_lane, int forced, int n) {
   if (forced >= 0) return forced;
   int lg = 0;
-  while (lg < 3 && (double)(1 << lg) * dz < h_lane && (64 << lg) <= n + 31) ++lg;  // 2^(lg+1) warps busy
+  // 2^(lg+1) warps busy, and 2^(lg+1) warps must exist in the CTA
+  while (lg < 3 && (double)(1 << lg) * dz < h_lane && (64 << lg) <= n + 31 && (64 << lg) <= kV2Threads) ++lg;
   return lg;
 }
 __device__ __forceinline__ int member_of(int tid, int lg) {
@@ -188,7 +192,8 @@ struct Physics {
   float scl[G];
   const uint8_t* mat;
   const float* qt;
-  int cb;  // first cell of the current chunk (tile cell 0)
+  int cb;        // first cell of the current chunk (tile cell 0)
+  int tile_off;  // byte offset of the tile in the dynamic buffer
 #ifdef MOC_DEBUG_WALK
   int dbg_lo, dbg_hi, dbg_dir;
 #endif
@@ -203,7 +208,7 @@ struct Physics {
 #endif
     extern __shared__ __align__(16) uint8_t dsm[];
     const int x = pc - cb;
-    uint32_t* cell = reinterpret_cast<uint32_t*>(dsm + tile_words_offset(GP)) + x * (GP + 1);
+    uint32_t* cell = reinterpret_cast<uint32_t*>(dsm + tile_off) + x * (GP + 1);
     atomicAdd(cell + GP, 1u);
     float sg[GP];
     if constexpr (GP % 4 == 0) {
@@ -246,9 +251,10 @@ struct WalkState {
   float pq[GP];
 
   __device__ __forceinline__ void load(const KSeg& e) {
-    s_rad = e.s;
-    kx = e.kx;
-    ky = e.ky;
+    const int4 v = *reinterpret_cast<const int4*>(&e);  // one LDS.128
+    s_rad = __hiloint2double(v.y, v.x);
+    kx = v.z;
+    ky = v.w;
   }
   // make raw piece (k, l) the pending segment: its cell, source and material
   __device__ __forceinline__ void set_pending(int jx, int cy, int ll, const uint8_t* mat, const float* qt) {
@@ -449,7 +455,7 @@ template <int G, int GP, bool HYBRID>
 __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a) {
   extern __shared__ __align__(16) uint8_t dsm[];
   const int cap = a.cap_cells;
-  uint32_t* const cells = reinterpret_cast<uint32_t*>(dsm + tile_words_offset(GP));  // [cap][GP + 1]
+  uint32_t* const cells = reinterpret_cast<uint32_t*>(dsm + a.tile_off);  // [cap][GP + 1]
   __shared__ uint32_t s_unit;
   __shared__ int s_nchunk;
 
@@ -484,8 +490,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const double z0b = d.st_z0[s];
     const double zf = z0b + (double)U.i0 * dz, zl = z0b + (double)(U.i0 + U.n - 1) * dz;
     // per-unit tables at the top of the dynamic buffer, the tile below them
-    const int tab0 = (a.dyn_bytes - unit_table_bytes(nk)) & ~15;
-    KSeg* const TF = reinterpret_cast<KSeg*>(dsm + tab0);
+    KSeg* const TF = reinterpret_cast<KSeg*>(dsm);
     KSeg* const TB = TF + nk;
     int* const base = reinterpret_cast<int*>(TB + nk);
     int* const chunk = base + nk + 1;
@@ -589,6 +594,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     for (int g = 0; g < G; ++g) ph.scl[g] = sh_scale[g];
     ph.mat = a.mat;
     ph.qt = a.qt;
+    ph.tile_off = a.tile_off;
     const double tn = d.an_tan[an], isn = d.an_invsin[an], Lt = d.t_len[t];
     const double z0 = z0b + (double)(U.i0 + p) * dz;
     const bool up = cot > 0;
