@@ -589,10 +589,20 @@ void run_sweep(moc_solver* s) {
     a.unit_exp = s->d_unit_exp;
     a.store = s->d_store;
     a.cost = s->d_cost;
-    if (s->d_unit_exp)
+    // EXP (§4.2): the preloaded units are a prefix of the cost-sorted list; replay them,
+    // then sweep the rest on the fly (each kernel pulls from its own counter)
+    const uint32_t n_exp = (uint32_t)s->exp_units;
+    if (n_exp) {
+      a.n_units = n_exp;
       k_sweep_v2<G, GP, true><<<s->sweep_blocks, kV2Threads, s->v2_smem, s->stream>>>(a);
-    else
+    }
+    if (s->n_units > n_exp) {
+      a.units = s->d_units + n_exp;
+      a.unit_exp = nullptr;
+      a.n_units = s->n_units - n_exp;
+      a.counter = s->d_counter + 1;
       k_sweep_v2<G, GP, false><<<s->sweep_blocks, kV2Threads, s->v2_smem, s->stream>>>(a);
+    }
   } else {
     k_sweep_v1<G, GP><<<s->sweep_blocks, s->sweep_threads, 0, s->stream>>>(
         s->dd, s->d_work, s->nwork, s->d_link, s->d_mat, s->d_qt, s->d_psi[in], s->d_psi[out], s->d_tally, s->d_sc);
@@ -637,7 +647,7 @@ void iter_sweep_half(moc_solver* s, bool time_it) {
     k_region_qmax<G, GP><<<64, 256, 0, s->stream>>>(s->J / s->NL, s->NL, s->d_qt, s->d_rmax);
     k_track_qmax<G, GP><<<64, 256, 0, s->stream>>>(s->T2, s->d_t_seg, s->d_seg_region, s->d_rmax, s->d_qmax_t);
     CUDA_OK(cudaMemsetAsync(s->d_tally32, 0, sizeof(float) * s->J * s->GP, s->stream));
-    CUDA_OK(cudaMemsetAsync(s->d_counter, 0, sizeof(uint32_t), s->stream));
+    CUDA_OK(cudaMemsetAsync(s->d_counter, 0, 2 * sizeof(uint32_t), s->stream));
   } else {
     CUDA_OK(cudaMemsetAsync(s->d_tally, 0, sizeof(double) * s->J * s->GP, s->stream));
   }
@@ -1033,7 +1043,7 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
           CUDA_OK(cudaStreamSynchronize(st));
         }
       }
-      s->d_counter = dmalloc<uint32_t>(1, B);
+      s->d_counter = dmalloc<uint32_t>(2, B);  // OTF and EXP unit queues
       s->d_err = dmalloc<int>(1, B);
       CUDA_OK(cudaMemsetAsync(s->d_err, 0, sizeof(int), st));
       s->d_rmax = dmalloc<float>((size_t)g.n_regions * s->GP, B);
@@ -1274,7 +1284,8 @@ int moc_get_timings(moc_solver* s, moc_timings* t) {
   t->iter_ms_last = s->iter_ms_last;
   // kernels per iteration: source, sweep, finalize, keff, normalize, resid (+ the two
   // bound kernels for schedule 0, + halo gather/scatter and leak park/restore for world > 1)
-  t->launches_per_iter = 6 + (s->opts.schedule == 0 ? 2 : 0) + (s->comm.world > 1 ? 4 : 0);
+  t->launches_per_iter = 6 + (s->opts.schedule == 0 ? 2 : 0) + (s->comm.world > 1 ? 4 : 0) +
+                         (s->exp_units > 0 && (int64_t)s->n_units > s->exp_units ? 1 : 0);  // EXP + OTF sweeps
   t->setup_ms = s->setup_ms;
   t->device_bytes = s->dev_bytes;
   t->exp_segments = s->exp_segments;

@@ -80,7 +80,7 @@ struct Unit {
 };
 
 // merged segment record: meta = kk | layer << 10 | material << 18, plus the 3D length
-struct Rec {
+struct __align__(8) Rec {
   uint32_t meta;
   float L;
 };
@@ -389,28 +389,55 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, G
   }
 }
 
-// Replay of a record stream (stride kV2Threads between a thread's consecutive records),
-// records [q0, q1) in direction dq = +1 (forward) or -1 (backward), one record of
-// look-ahead (record and source loaded before the current one is applied).
+// Replay of a record stream (stride kV2Threads between a thread's consecutive records)
+// in direction dq = +1 (forward) or -1 (backward).  Records are loaded kRecAhead ahead
+// (HBM latency) and the next record's source one ahead, so the chain record -> table ->
+// source never stalls the Eq. 3 work of the current record.
+constexpr int kRecAhead = 4;
 template <int GP>
 struct Replay {
   const Rec* rs;
   const KSeg* TF;
-  int q, qend, dq;  // next record to apply; stop index (exclusive)
-  Rec cur;
-  int cpc;
-  float cq[GP];
+  int q, dq;     // next record index to load; step
+  int n_load;    // records still to load
+  int n_left;    // records still to apply
+  Rec buf[kRecAhead];  // buf[0] = next to apply
+  int cpc;       // tile cell of buf[0]
+  float cq[GP];  // source of buf[0]
   bool valid;
 
-  __device__ __forceinline__ void fetch(const float* qt) {
-    valid = q != qend;
+  __device__ __forceinline__ Rec load_next() {
+    Rec x{0u, 0.f};
+    if (n_load > 0) {
+      x = rs[(size_t)q * kV2Threads];
+      q += dq;
+      --n_load;
+    }
+    return x;
+  }
+  __device__ __forceinline__ void prepare(const float* qt) {
+    valid = n_left > 0;
     if (valid) {
-      cur = rs[(size_t)q * kV2Threads];
-      const int kk = cur.meta & 1023, l = (cur.meta >> 10) & 255;
+      const int kk = buf[0].meta & 1023, l = (buf[0].meta >> 10) & 255;
       const KSeg e = TF[kk];
       cpc = e.ky + l;
       load_q<GP>(qt, (int64_t)(e.kx + l), cq);
     }
+  }
+  __device__ __forceinline__ void start(int q0, int nrec, const float* qt) {
+    q = q0;
+    n_load = nrec;
+    n_left = nrec;
+#pragma unroll
+    for (int i = 0; i < kRecAhead; ++i) buf[i] = load_next();
+    prepare(qt);
+  }
+  __device__ __forceinline__ void advance(const float* qt) {
+#pragma unroll
+    for (int i = 0; i + 1 < kRecAhead; ++i) buf[i] = buf[i + 1];
+    buf[kRecAhead - 1] = load_next();
+    --n_left;
+    prepare(qt);
   }
 };
 
@@ -418,16 +445,15 @@ struct Replay {
 template <int G, int GP>
 __device__ __forceinline__ void replay_chunk(Replay<GP>& r, Physics<G, GP>& ph, int k_lo, int k_hi) {
   while (r.valid) {
-    const int kk = r.cur.meta & 1023;
+    const Rec cur = r.buf[0];
+    const int kk = cur.meta & 1023;
     if (kk < k_lo || kk >= k_hi) return;
-    const int m = r.cur.meta >> 18, pc = r.cpc;
-    const float L = r.cur.L;
+    const int m = cur.meta >> 18, pc = r.cpc;
     float q[GP];
 #pragma unroll
     for (int h = 0; h < GP; ++h) q[h] = r.cq[h];
-    r.q += r.dq;
-    r.fetch(ph.qt);  // look-ahead load overlaps the physics below
-    ph.emit(pc, m, q, L);
+    r.advance(ph.qt);  // look-ahead loads overlap the physics below
+    ph.emit(pc, m, q, cur.L);
   }
 }
 
@@ -449,9 +475,10 @@ __device__ __forceinline__ int k_of_cell(const int* base, int k_lo, int k_hi, in
   return lo;
 }
 
-// HYBRID = false: pure on-the-fly sweep (the replay path is not compiled in, which keeps
-// the register budget for the walk); true: units may be EXP-preloaded.
-template <int G, int GP, bool HYBRID>
+// EXP = false: on-the-fly sweep of the units past the preloaded prefix (the replay path
+// is not compiled in, which keeps the register budget for the walk); EXP = true: replay
+// of the preloaded units (§4.2), no walk code.  The two run back to back on the stream.
+template <int G, int GP, bool EXP>
 __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a) {
   extern __shared__ __align__(16) uint8_t dsm[];
   const int cap = a.cap_cells;
@@ -480,7 +507,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const uint32_t u = s_unit;
     if (u >= a.n_units) break;
     const Unit U = a.units[u];
-    const uint64_t exp_off = HYBRID ? a.unit_exp[u] : kNoExp;
+    const uint64_t exp_off = EXP ? a.unit_exp[u] : kNoExp;
     const int s = (int)U.stack;
     const int t = s / d.N, n = s - t * d.N;
     const int an = d.t_a[t] * d.N + n;
@@ -599,9 +626,9 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const double z0 = z0b + (double)(U.i0 + p) * dz;
     const bool up = cot > 0;
     const float cw = d.an_c[an];
-    const bool otf = !HYBRID || exp_off == kNoExp;
+    constexpr bool otf = !EXP;
     double s_in = 0, s_out = 0;
-    if (otf) {
+    if constexpr (otf) {
       TrackGeo tg;
       tg.z0 = z0;
       tg.cot = cot;
@@ -620,7 +647,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         ph.psi[g] = active ? a.psi_in[(size_t)(2 * id + dir) * GP + g] * ps * ph.scl[g] : 0.f;
       WalkState<G, GP> w;
       Replay<GP> r;
-      if (otf) {
+      if constexpr (otf) {
         w.done = !active;
         w.carry = 0.f;
         w.pc = -1;
@@ -658,10 +685,8 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const int nrec = active ? (int)a.cost[id] : 0;
         r.rs = a.store + exp_off + tid;
         r.TF = TF;
-        r.q = dir == 0 ? 0 : nrec - 1;
-        r.qend = dir == 0 ? nrec : -1;
         r.dq = dir == 0 ? 1 : -1;
-        r.fetch(a.qt);
+        r.start(dir == 0 ? 0 : nrec - 1, nrec, a.qt);
       }
 #pragma unroll 1
       for (int ci = 0; ci < nchunk; ++ci) {
@@ -674,7 +699,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         ph.dbg_hi = ce;
         ph.dbg_dir = dir;
 #endif
-        if (!otf) replay_chunk(r, ph, k_lo, k_hi);
+        if constexpr (!otf) replay_chunk(r, ph, k_lo, k_hi);
         else if (up) walk_chunk<G, GP, true>(dir, w, ph, TF, TB, z0, tn, isn, cb, ce);
         else walk_chunk<G, GP, false>(dir, w, ph, TF, TB, z0, tn, isn, cb, ce);
         __syncthreads();
