@@ -106,6 +106,16 @@ def _dist_env():
     return rank, world, local
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical CPUs visible)"
+    except OSError:
+        pass
+    return None
+
+
 def oracle_sample(prob, target_s: float = 15.0):
     """Time the oracle as it stands on a bounded sample of the workload's tracks:
     every `stride`-th 3D track, swept once in both directions (re-traced explicitly)."""
@@ -119,7 +129,7 @@ def oracle_sample(prob, target_s: float = 15.0):
         stride = max(1, int(stride * sec / target_s))
     sec, nint = o.time_sample_sweep(stride)
     threads = oracle.num_threads()
-    return dict(value=nint / sec, unit=UNIT, cores=threads, kind="oracle",
+    return dict(value=nint / sec, unit=UNIT, cores=threads, kind="oracle", cpu_model=_cpu_model(),
                 sample=f"every {stride}th of {n3} 3D tracks ({(n3 + stride - 1) // stride} tracks, "
                        f"{nint:.3e} integrations, fp64, explicit re-trace + sweep, {sec:.1f} s on {threads} threads)",
                 seconds=sec, integrations=nint)
@@ -164,7 +174,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C5G7-shaped XS, problems/)",
         "config": {"workload": WORKLOADS.get(args.config, f"cfg{args.config}"), "sample": base["sample"]},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": base["cores"], "kind": "oracle",
-                         "sample": base["sample"]},
+                         "sample": base["sample"], "cpu_model": base.get("cpu_model")},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -254,7 +264,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = oracle_sample(prob, target_s=args.ref_seconds)
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}.json")
     if os.path.exists(tp):
@@ -296,7 +306,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)  # median over >= 20 iterations
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
