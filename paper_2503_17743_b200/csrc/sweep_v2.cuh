@@ -117,14 +117,14 @@ struct V2Args {
 // SIMT lanes: lane efficiency 0.90 contiguous vs 0.76 spread over the band on cfg4,
 // tools/lane_eff.py) but cross the same FSR at the same time (same-address shared
 // atomics serialise); the stride trades the two.  lane_lg_of picks it per unit from the
-// stack's member spacing dz: the smallest 2^lg (<= 8) with 2^lg dz >= h_min / 3 (about
+// stack's member spacing dz: the smallest 2^lg (<= warps per CTA) with 2^lg dz >= h_min / 3 (about
 // 3 lanes per layer thickness) while 2^lg warps stay busy on the band's n members
 // (A/B over the divisor and forced strides on cfg4 / cfg5: profiles/README.md).
 __device__ __forceinline__ int lane_lg_of(double dz, double h_lane, int forced, int n) {
   if (forced >= 0) return forced;
   int lg = 0;
   // 2^(lg+1) warps busy, and 2^(lg+1) warps must exist in the CTA
-  while (lg < 3 && (double)(1 << lg) * dz < h_lane && (64 << lg) <= n + 31 && (64 << lg) <= kV2Threads) ++lg;
+  while ((64 << lg) <= kV2Threads && (double)(1 << lg) * dz < h_lane && (64 << lg) <= n + 31) ++lg;
   return lg;
 }
 __device__ __forceinline__ int member_of(int tid, int lg) {
