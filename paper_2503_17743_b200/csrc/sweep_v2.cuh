@@ -481,7 +481,8 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
   __shared__ uint32_t s_unit;
   __shared__ int s_nchunk;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = kV2Threads / 32;
   const DevData& d = a.d;
   for (int q = tid; q < kMaxMat * GP; q += blockDim.x) {
     const int m = q / GP, g = q - m * GP;
@@ -702,7 +703,10 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         //    reductions), re-zeroing every consumed cell.  Each warp takes a contiguous
         //    eighth of the chunk's cells, lane-strided, so a lane's 2D segment k (for the
         //    cell's FSR) advances by a step or two per cell from one binary search.
-        const int per = (ce - cb + nw - 1) / nw;
+        const int per = (ce - cb + nw - 1) / nw;  // nw is a compile-time constant
+        float fsc[G];  // fixed point -> c_{a,n} * dpsi, per group
+#pragma unroll
+        for (int g = 0; g < G; ++g) fsc[g] = sh_iscale[g] * cw;
         const int x1 = min(ce - cb, (warp + 1) * per);
         int kc = -1;
         for (int x = warp * per + lane; x < x1; x += 32) {
@@ -723,7 +727,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
           }
           float val[GP];
 #pragma unroll
-          for (int g = 0; g < GP; ++g) val[g] = g < G ? (float)(int)(raw[g] - cnt * kMagicBits) * (sh_iscale[g] * cw) : 0.f;
+          for (int g = 0; g < GP; ++g) val[g] = g < G ? (float)(int)(raw[g] - cnt * kMagicBits) * fsc[g] : 0.f;
           float* dst = a.tally + j * GP;
           if constexpr (GP % 4 == 0) {
 #pragma unroll
