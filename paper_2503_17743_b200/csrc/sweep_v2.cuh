@@ -698,6 +698,9 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         if constexpr (!otf) replay_chunk(r, ph, k_lo, k_hi);
         else if (up) walk_chunk<G, GP, true>(dir, w, ph, TF, TB, z0, tn, isn, cb, ce);
         else walk_chunk<G, GP, false>(dir, w, ph, TF, TB, z0, tn, isn, cb, ce);
+        // the forward pass's last chunk is the backward pass's first: keep accumulating
+        // (tile atomics commute) and flush both directions' sums once
+        if (dir == 0 && ci == nchunk - 1) continue;
         __syncthreads();
         // 4. flush the chunk: c_{a,n} * fixed-point sums -> global tally (fp32 vector
         //    reductions), re-zeroing every consumed cell.  Each warp takes a contiguous
