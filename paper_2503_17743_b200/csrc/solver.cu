@@ -441,6 +441,15 @@ __global__ void k_leak_park(double* sc, float* tail, int dir) {
   }
 }
 
+// phi f32 [J][GP] -> f64 [J][G] (the host API's layout), so moc_get_scalar_flux is one
+// device-side conversion and one DMA into the caller's buffer
+__global__ void k_phi_f64(const float* phi, int64_t J, int G, int GP, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < J * G; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i / G;
+    out[i] = (double)phi[j * GP + (i - j * G)];
+  }
+}
+
 __global__ void k_fill_f32(float* p, int64_t n, float v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
@@ -488,6 +497,7 @@ struct moc_solver {
   uint32_t* d_cost = nullptr;
   uint8_t* d_mat = nullptr;
   float *d_qt = nullptr, *d_phi = nullptr, *d_fold = nullptr, *d_fnew = nullptr;
+  double* d_phi64 = nullptr;  // [J][G] staging for moc_get_scalar_flux (allocated on first use)
   double *d_tally = nullptr, *d_vol = nullptr;
   float* d_psi[2] = {nullptr, nullptr};
   double *d_sc = nullptr, *d_part_a = nullptr, *d_part_b = nullptr, *d_part_c = nullptr, *d_hist = nullptr;
@@ -768,7 +778,7 @@ void destroy(moc_solver* s) {
                   s->d_link, s->d_work, s->d_cost, s->d_mat, s->d_qt, s->d_phi, s->d_fold, s->d_fnew, s->d_tally,
                   s->d_vol, s->d_psi[0], s->d_psi[1], s->d_sc, s->d_part_a, s->d_part_b, s->d_part_c, s->d_hist,
                   s->d_units, s->d_counter, s->d_rmax, s->d_qmax_t, s->d_tally32, s->d_err,
-                  s->d_unit_maxq, s->d_unit_exp, s->d_store};
+                  s->d_unit_maxq, s->d_unit_exp, s->d_store, s->d_phi64};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : s->ev)
@@ -1190,11 +1200,12 @@ int moc_solver_update_materials(moc_solver* s, const double* sigma_t, const doub
 int moc_get_scalar_flux(moc_solver* s, double* phi) {
   if (!s || !phi) return MOC_E_INVALID_ARG;
   SOLVER_TRY(s, {
-    std::vector<float> h((size_t)s->J * s->GP);
-    CUDA_OK(cudaMemcpyAsync(h.data(), s->d_phi, 4 * h.size(), cudaMemcpyDeviceToHost, s->stream));
+    const size_t n = (size_t)s->J * s->G;
+    if (!s->d_phi64) s->d_phi64 = dmalloc<double>(n, s->dev_bytes);
+    k_phi_f64<<<s->nb_fsr, 256, 0, s->stream>>>(s->d_phi, s->J, s->G, s->GP, s->d_phi64);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpyAsync(phi, s->d_phi64, 8 * n, cudaMemcpyDeviceToHost, s->stream));
     CUDA_OK(cudaStreamSynchronize(s->stream));
-    for (int64_t j = 0; j < s->J; ++j)
-      for (int g = 0; g < s->G; ++g) phi[j * s->G + g] = h[j * s->GP + g];
   })
 }
 
