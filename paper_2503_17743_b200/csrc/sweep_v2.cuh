@@ -710,23 +710,22 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         float fsc[G];  // fixed point -> c_{a,n} * dpsi, per group
 #pragma unroll
         for (int g = 0; g < G; ++g) fsc[g] = sh_iscale[g] * cw;
-        const int x1 = min(ce - cb, (warp + 1) * per);
-        int kc = -1;
-        for (int x = warp * per + lane; x < x1; x += 32) {
+        const int x0 = warp * per + lane, x1 = min(ce - cb, (warp + 1) * per);
+        int kc = x0 < x1 ? k_of_cell(base, k_lo, k_hi, cb + x0) : k_lo;
+        for (int x = x0; x < x1; x += 32) {
           uint32_t* cp = cells + (size_t)x * (GP + 1);
           const uint32_t cnt = cp[GP];
           if (!cnt) continue;
           cp[GP] = 0u;
           nemit += cnt;
-          if (kc < 0) kc = k_of_cell(base, k_lo, k_hi, cb + x);
           while (base[kc + 1] <= cb + x) ++kc;
           const KSeg e = TF[kc];
           const int64_t j = (int64_t)(e.kx - e.ky) + cb + x;  // FSR of cell cb + x = ky + layer
           uint32_t raw[GP];
 #pragma unroll
           for (int g = 0; g < GP; ++g) {
-            raw[g] = cp[g];
-            cp[g] = 0u;
+            raw[g] = g < G ? cp[g] : kMagicBits * cnt;  // pad words are never written
+            if (g < G) cp[g] = 0u;
           }
           float val[GP];
 #pragma unroll
