@@ -132,6 +132,14 @@ __device__ __forceinline__ int member_of(int tid, int lg) {
   return ((w >> lg) << (5 + lg)) + (lane << lg) + (w & ((1 << lg) - 1));
 }
 
+// a value the compiler must keep in a register rather than re-derive at every use (it
+// otherwise recomputes shared-window bases from SR_CgaCtaId inside the hot loop)
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float e) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(e)
                : "memory");
@@ -186,17 +194,41 @@ __device__ __forceinline__ int kseg_upto(const KSeg* T, int nk, double s) {
 // fixed-point units (psi' = psi * scale_g, scale_g = 2^21 / bound_g), so the tally term
 // dpsi' = (psi' - q scale_g)(1 - e^{-tau}) is already scaled and its fixed-point code is
 // one FADD with the 1.5 * 2^23 magic: per group FMUL, MUFU.EX2, 2 FFMA, 2 FADD, ATOMS.
+// MOC_V2_PACKED pairs the groups with Blackwell's packed fp32 instructions (FMUL2 / FFMA2 /
+// FADD2; a pair then costs 9 issue slots instead of 14, the hot loop 116 instead of 128
+// instructions) but measured slower (cfg4 22.07 vs 20.87 ms, cfg5 165.6 vs 159.2 ms):
+// FFMA2 holds the FMA pipe for two cycles (profiles/micro_r2.jsonl: same 122 FMA/clk/SM as
+// FFMA) and the kernel is latency-, not issue-bound.  Storage is in pairs either way; for
+// odd G the last pair's upper half is a dead lane (scale 0, psi 0).
 template <int G, int GP>
 struct Physics {
-  float psi[G];
-  float scl[G];
+  static constexpr int NP = (G + 1) / 2;
+  float2 psi2[NP];
+  float2 scl2[NP];
   const uint8_t* mat;
   const float* qt;
   int cb;        // first cell of the current chunk (tile cell 0)
   int tile_off;  // byte offset of the tile in the dynamic buffer
+  uint32_t tsa;  // shared address of the tile minus cb cells (cell pc at tsa + pc * 4 (GP + 1))
+  uint32_t ssa;  // shared address of sh_sig
+  uint32_t psa;  // shared address of sh_planes
+
+  // axial plane i (an LDS.64 from the register-held base)
+  __device__ __forceinline__ double plane(int i) const {
+#ifndef MOC_V2_GENERIC_SMEM
+    double z;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(z) : "r"(psa + 8u * (uint32_t)i));
+    return z;
+#else
+    return sh_planes[i];
+#endif
+  }
 #ifdef MOC_DEBUG_WALK
   int dbg_lo, dbg_hi, dbg_dir;
 #endif
+
+  __device__ __forceinline__ float& psi(int g) { return (g & 1) ? psi2[g >> 1].y : psi2[g >> 1].x; }
+  __device__ __forceinline__ float& scl(int g) { return (g & 1) ? scl2[g >> 1].y : scl2[g >> 1].x; }
 
   __device__ __forceinline__ void emit(int pc, int m, const float* q, float Lf) {
 #ifdef MOC_DEBUG_WALK
@@ -206,6 +238,26 @@ struct Physics {
       return;
     }
 #endif
+#ifndef MOC_V2_GENERIC_SMEM
+    // 32-bit shared-window addresses held in registers (tile base pre-offset by the
+    // chunk's first cell; Sigma_t table base): one IMAD / LEA per emit instead of the
+    // compiler re-deriving both generic->shared bases (S2UR CgaCtaId, ULEA, LDC) each time
+    const uint32_t ca = tsa + (uint32_t)pc * (4u * (GP + 1));
+    asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(ca), "n"(4 * GP));
+    float sg[GP];
+    if constexpr (GP % 4 == 0) {
+#pragma unroll
+      for (int h = 0; h < GP / 4; ++h)
+        asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+            : "=f"(sg[4 * h]), "=f"(sg[4 * h + 1]), "=f"(sg[4 * h + 2]), "=f"(sg[4 * h + 3])
+            : "r"(ssa + (uint32_t)m * (4u * GP) + 16u * h));
+    } else {
+#pragma unroll
+      for (int h = 0; h < GP; ++h)
+        asm("ld.shared.f32 %0, [%1];" : "=f"(sg[h]) : "r"(ssa + (uint32_t)m * (4u * GP) + 4u * h));
+    }
+#define MOC_TILE_ADD(g, v) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(ca + 4u * (g)), "r"(v))
+#else
     extern __shared__ __align__(16) uint8_t dsm[];
     const int x = pc - cb;
     uint32_t* cell = reinterpret_cast<uint32_t*>(dsm + tile_off) + x * (GP + 1);
@@ -224,14 +276,37 @@ struct Physics {
 #pragma unroll
       for (int h = 0; h < GP; ++h) sg[h] = sh_sig[m * GP + h];
     }
+#define MOC_TILE_ADD(g, v) atomicAdd(cell + (g), (v))
+#endif
+#ifndef MOC_V2_PACKED
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const float E = ex2_approx(-sg[g] * Lf);
-      const float dd = fmaf(-q[g], scl[g], psi[g]);
+      const float dd = fmaf(-q[g], scl(g), psi(g));
       const float dl = fmaf(-dd, E, dd);  // (psi' - q')(1 - E)
-      psi[g] -= dl;
-      atomicAdd(cell + g, __float_as_uint(dl + kMagic));
+      psi(g) -= dl;
+      MOC_TILE_ADD(g, __float_as_uint(dl + kMagic));
     }
+#else
+    const float2 nL = make_float2(-Lf, -Lf);
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const int g0 = 2 * i, g1 = 2 * i + 1;
+      const float2 sp = make_float2(sg[g0], g1 < GP ? sg[g1] : 0.f);
+      const float2 qp = make_float2(-q[g0], g1 < GP ? -q[g1] : 0.f);
+      const float2 ta = __fmul2_rn(sp, nL);  // -sigma_t log2(e) L
+      float2 E;
+      E.x = ex2_approx(ta.x);
+      E.y = g1 < G ? ex2_approx(ta.y) : 0.f;
+      const float2 dd = __ffma2_rn(qp, scl2[i], psi2[i]);                      // psi' - q'
+      const float2 dl = __ffma2_rn(make_float2(-dd.x, -dd.y), E, dd);          // (psi' - q')(1 - E)
+      psi2[i] = __fadd2_rn(psi2[i], make_float2(-dl.x, -dl.y));
+      const float2 code = __fadd2_rn(dl, make_float2(kMagic, kMagic));
+      MOC_TILE_ADD(g0, __float_as_uint(code.x));
+      if (g1 < G) MOC_TILE_ADD(g1, __float_as_uint(code.y));
+    }
+#endif
+#undef MOC_TILE_ADD
   }
 };
 
@@ -317,13 +392,13 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
         w.load(TF[w.k]);
       } else {
         w.l += UP ? 1 : -1;
-        w.s_ax = (sh_planes[w.l + (UP ? 1 : 0)] - z0) * tn;
+        w.s_ax = (ph.plane(w.l + (UP ? 1 : 0)) - z0) * tn;
       }
 #else
       w.k += rad ? 1 : 0;
       w.l += rad ? 0 : (UP ? 1 : -1);
       w.load(TF[w.k]);
-      w.s_ax = (sh_planes[w.l + (UP ? 1 : 0)] - z0) * tn;
+      w.s_ax = (ph.plane(w.l + (UP ? 1 : 0)) - z0) * tn;
 #endif
     }
   }
@@ -377,13 +452,13 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, G
         w.load(TB[w.k]);
       } else {
         w.l -= UP ? 1 : -1;
-        w.s_ax = (sh_planes[w.l + (UP ? 0 : 1)] - z0) * tn;
+        w.s_ax = (ph.plane(w.l + (UP ? 0 : 1)) - z0) * tn;
       }
 #else
       w.k -= rad ? 1 : 0;
       w.l -= rad ? 0 : (UP ? 1 : -1);
       w.load(TB[w.k]);
-      w.s_ax = (sh_planes[w.l + (UP ? 0 : 1)] - z0) * tn;
+      w.s_ax = (ph.plane(w.l + (UP ? 0 : 1)) - z0) * tn;
 #endif
     }
   }
@@ -614,10 +689,13 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     __syncthreads();
     const int nchunk = s_nchunk;
 #pragma unroll
-    for (int g = 0; g < G; ++g) ph.scl[g] = sh_scale[g];
+    for (int g = 0; g < 2 * Physics<G, GP>::NP; ++g) ph.scl(g) = g < G ? sh_scale[g] : 0.f;
     ph.mat = a.mat;
     ph.qt = a.qt;
     ph.tile_off = a.tile_off;
+    const uint32_t tile_sa = (uint32_t)__cvta_generic_to_shared(dsm) + (uint32_t)a.tile_off;
+    ph.ssa = opaque_u32((uint32_t)__cvta_generic_to_shared(sh_sig));
+    ph.psa = opaque_u32((uint32_t)__cvta_generic_to_shared(sh_planes));
     const double tn = d.an_tan[an], isn = d.an_invsin[an], Lt = d.t_len[t];
     const double z0 = z0b + (double)(U.i0 + p) * dz;
     const bool up = cot > 0;
@@ -639,8 +717,8 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
 #pragma unroll 1
     for (int dir = 0; dir < 2; ++dir) {
 #pragma unroll
-      for (int g = 0; g < G; ++g)
-        ph.psi[g] = active ? a.psi_in[(size_t)(2 * id + dir) * GP + g] * ps * ph.scl[g] : 0.f;
+      for (int g = 0; g < 2 * Physics<G, GP>::NP; ++g)
+        ph.psi(g) = active && g < G ? a.psi_in[(size_t)(2 * id + dir) * GP + g] * ps * ph.scl(g) : 0.f;
       WalkState<G, GP> w;
       Replay<GP> r;
       if constexpr (otf) {
@@ -690,6 +768,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const int k_lo = chunk[c], k_hi = chunk[c + 1];
         const int cb = base[k_lo], ce = base[k_hi];
         ph.cb = cb;
+        ph.tsa = opaque_u32(tile_sa - (uint32_t)cb * (4u * (GP + 1)));
 #ifdef MOC_DEBUG_WALK
         ph.dbg_lo = cb;
         ph.dbg_hi = ce;
@@ -746,11 +825,11 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const uint32_t out = a.link[2 * id + dir];
         if (out != 0xffffffffu) {
 #pragma unroll
-          for (int g = 0; g < G; ++g) a.psi_out[(size_t)out * GP + g] = ph.psi[g] * sh_iscale[g];
+          for (int g = 0; g < G; ++g) a.psi_out[(size_t)out * GP + g] = ph.psi(g) * sh_iscale[g];
         } else {
           float e = 0.f;
 #pragma unroll
-          for (int g = 0; g < G; ++g) e += ph.psi[g] * sh_iscale[g];
+          for (int g = 0; g < G; ++g) e += ph.psi(g) * sh_iscale[g];
           leak += (double)(cw * e);
         }
       }

@@ -42,6 +42,45 @@ __global__ void k_ffma(float* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+
+// Blackwell packed fp32 (FFMA2): 8 independent chains of fma.rn.f32x2 per thread.
+__global__ void k_ffma2(float* out, int iters) {
+  unsigned long long a[8];
+  for (int j = 0; j < 8; ++j) { float2 f = make_float2(threadIdx.x * 1e-3f + j, j * 0.5f); a[j] = *(unsigned long long*)&f; }
+  float2 cm = make_float2(0.999f, 0.998f), ca = make_float2(0.001f, 0.002f);
+  unsigned long long m = *(unsigned long long*)&cm, c = *(unsigned long long*)&ca;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[j]) : "l"(m), "l"(c));
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+  float s = 0; for (int j = 0; j < 8; ++j) { float2 f = *(float2*)&a[j]; s += f.x + f.y; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// FFMA2 interleaved 1:1 with integer adds: are packed ops issue-limited or pipe-limited?
+__global__ void k_ffma2_iadd(float* out, int iters) {
+  unsigned long long a[4];
+  unsigned b[4];
+  for (int j = 0; j < 4; ++j) { float2 f = make_float2(threadIdx.x * 1e-3f + j, j * 0.5f); a[j] = *(unsigned long long*)&f; b[j] = threadIdx.x + j; }
+  float2 cm = make_float2(0.999f, 0.998f), ca = make_float2(0.001f, 0.002f);
+  unsigned long long m = *(unsigned long long*)&cm, c = *(unsigned long long*)&ca;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[j]) : "l"(m), "l"(c));
+      asm volatile("add.u32 %0, %0, %1;" : "+r"(b[j]) : "r"(j + 1));
+    }
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) g_cycles[blockIdx.x] = t1 - t0;
+  float s = 0; for (int j = 0; j < 4; ++j) { float2 f = *(float2*)&a[j]; s += f.x + f.y + b[j]; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void k_dfma(double* out, int iters) {
   double a[8];
   for (int j = 0; j < 8; ++j) a[j] = threadIdx.x * 1e-3 + j;
@@ -226,6 +265,11 @@ int main() {
     CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1); report("mufu_ex2", ms, 4.0 * it * B * T, B); }
   { int it = 20000; k_ffma<<<B, T>>>(out, 10); cudaEventRecord(e0); k_ffma<<<B, T>>>(out, it); cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1); report("ffma", ms, 8.0 * it * B * T, B); }
+  { int it = 20000; k_ffma2<<<B, T>>>(out, 10); cudaEventRecord(e0); k_ffma2<<<B, T>>>(out, it); cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1); report("ffma2_fp32_fmas", ms, 16.0 * it * B * T, B);
+    report("ffma2_warp_insts_x32", ms, 8.0 * it * B * T, B); }
+  { int it = 20000; k_ffma2_iadd<<<B, T>>>(out, 10); cudaEventRecord(e0); k_ffma2_iadd<<<B, T>>>(out, it); cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1); report("ffma2_plus_iadd_thread_insts", ms, 8.0 * it * B * T, B); }
   { int it = 5000; k_dfma<<<B, T>>>((double*)out, 10); cudaEventRecord(e0); k_dfma<<<B, T>>>((double*)out, it); cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1); report("dfma", ms, 8.0 * it * B * T, B); }
   size_t sm = 8192 * 4;
