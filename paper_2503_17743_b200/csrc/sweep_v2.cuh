@@ -45,7 +45,18 @@ constexpr int kMaxPlanes = 256;               // axial planes staged in shared m
 constexpr uint32_t kMagicBits = 0x4B400000u;  // bits of 1.5 * 2^23
 constexpr float kMagic = 12582912.0f;         // 1.5 * 2^23
 constexpr float kFixOne = 2097152.0f;         // 2^21: max |term| in fixed point
-constexpr uint64_t kNoExp = ~0ull;            // unit not preloaded (on-the-fly)
+constexpr uint64_t kNoExp = ~0ull;
+#ifndef MOC_V2_Q128
+#define MOC_V2_Q128 0
+#endif
+// MOC_V2_NOCOUNT: tile words receive bits(dpsi' + 1.5 * 2^23) - 0x4B400000 (an IADD per
+// group) instead of the raw bits plus a per-cell count atomic removing the offset at the flush
+#ifndef MOC_V2_NOCOUNT
+#define MOC_V2_NOCOUNT 1
+#endif
+#ifndef MOC_V2_PSI_SCALAR
+#define MOC_V2_PSI_SCALAR 0  // 1: per-group 32-bit boundary-psi loads / stores (A/B)
+#endif            // unit not preloaded (on-the-fly)
 // epsilon_L in the constant bank: DSETP reads it as an operand, where the immediate form
 // would cost two uniform moves per raw piece (same value as otf.h kEpsL)
 __constant__ double c_epsL = kEpsL;
@@ -156,7 +167,13 @@ __device__ __forceinline__ float attenuation_dpsi(float psi, float q, float sig_
 
 template <int GP>
 __device__ __forceinline__ void load_q(const float* qt, int64_t j, float* q) {
-  if constexpr (GP % 4 == 0) {
+  if constexpr (GP == 8 && !MOC_V2_Q128) {
+    // one 256-bit load per FSR record (LDG.E.ENL2.256): half the load instructions and L1
+    // data-pipe wavefronts of two LDG.128 — the L1 data pipe is the sweep's busiest unit
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(q[0]), "=f"(q[1]), "=f"(q[2]), "=f"(q[3]), "=f"(q[4]), "=f"(q[5]), "=f"(q[6]), "=f"(q[7])
+        : "l"(qt + j * GP));
+  } else if constexpr (GP % 4 == 0) {
 #pragma unroll
     for (int h = 0; h < GP / 4; ++h) {
       const float4 x = __ldg(reinterpret_cast<const float4*>(qt + j * GP) + h);
@@ -212,6 +229,7 @@ struct Physics {
   uint32_t tsa;  // shared address of the tile minus cb cells (cell pc at tsa + pc * 4 (GP + 1))
   uint32_t ssa;  // shared address of sh_sig
   uint32_t psa;  // shared address of sh_planes
+  uint32_t nem;  // emissions (MOC_V2_NOCOUNT: the tile has no per-cell count)
 
   // axial plane i (an LDS.64 from the register-held base)
   __device__ __forceinline__ double plane(int i) const {
@@ -243,7 +261,9 @@ struct Physics {
     // chunk's first cell; Sigma_t table base): one IMAD / LEA per emit instead of the
     // compiler re-deriving both generic->shared bases (S2UR CgaCtaId, ULEA, LDC) each time
     const uint32_t ca = tsa + (uint32_t)pc * (4u * (GP + 1));
+#if !MOC_V2_NOCOUNT
     asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(ca), "n"(4 * GP));
+#endif
     float sg[GP];
     if constexpr (GP % 4 == 0) {
 #pragma unroll
@@ -256,7 +276,12 @@ struct Physics {
       for (int h = 0; h < GP; ++h)
         asm("ld.shared.f32 %0, [%1];" : "=f"(sg[h]) : "r"(ssa + (uint32_t)m * (4u * GP) + 4u * h));
     }
+#if MOC_V2_NOCOUNT
+    ++nem;
+#define MOC_TILE_ADD(g, v) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(ca + 4u * (g)), "r"((v) - kMagicBits))
+#else
 #define MOC_TILE_ADD(g, v) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(ca + 4u * (g)), "r"(v))
+#endif
 #else
     extern __shared__ __align__(16) uint8_t dsm[];
     const int x = pc - cb;
@@ -369,6 +394,13 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
     sn = last ? w.s_end : sn;
     const double L3d = (sn - w.s) * isn;
     const float L3 = (float)L3d;
+#ifdef MOC_V2_EARLY_ADVANCE
+    // MOC_V2_EARLY_ADVANCE: both candidate next crossings loaded before Eq. 3 (issue is in
+    // order, so their latency would hide under it; TF[nk] is TB[0]: a harmless read) —
+    // measured slower (cfg5 161.1 vs 157.9 ms: longer live ranges)
+    const int4 nv = *reinterpret_cast<const int4*>(&TF[w.k + 1]);
+    const double s_ax_n = (ph.plane(UP ? w.l + 2 : max(w.l - 1, 0)) - z0) * tn;
+#endif
     if (L3d < c_epsL) {
       if (w.pc >= 0) {
         w.pL += L3;  // a sliver merges into the segment before it
@@ -386,7 +418,17 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
       w.done = 1;
     } else {
       w.s = sn;
-#ifndef MOC_V2_BRANCHLESS
+#ifdef MOC_V2_EARLY_ADVANCE
+      if (rad) {
+        ++w.k;
+        w.s_rad = __hiloint2double(nv.y, nv.x);
+        w.kx = nv.z;
+        w.ky = nv.w;
+      } else {
+        w.l += UP ? 1 : -1;
+        w.s_ax = s_ax_n;
+      }
+#elif !defined(MOC_V2_BRANCHLESS)
       if (rad) {
         ++w.k;
         w.load(TF[w.k]);
@@ -433,6 +475,10 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, G
     sp = last ? w.s_end : sp;
     const double L3d = (w.s - sp) * isn;
     const float L3 = (float)L3d;
+#ifdef MOC_V2_EARLY_ADVANCE
+    const int4 nv = *reinterpret_cast<const int4*>(&TB[w.k - 1]);  // TB[-1] is TF[nk-1]: harmless
+    const double s_ax_n = (ph.plane(UP ? max(w.l - 1, 0) : w.l + 2) - z0) * tn;
+#endif
     if (L3d < c_epsL) {
       w.carry += L3;
       if (w.pc < 0) w.fkl = w.k | (w.l << 16);  // the forward-first sliver wins
@@ -446,7 +492,17 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, G
       w.done = 1;
     } else {
       w.s = sp;
-#ifndef MOC_V2_BRANCHLESS
+#ifdef MOC_V2_EARLY_ADVANCE
+      if (rad) {
+        --w.k;
+        w.s_rad = __hiloint2double(nv.y, nv.x);
+        w.kx = nv.z;
+        w.ky = nv.w;
+      } else {
+        w.l -= UP ? 1 : -1;
+        w.s_ax = s_ax_n;
+      }
+#elif !defined(MOC_V2_BRANCHLESS)
       if (rad) {
         --w.k;
         w.load(TB[w.k]);
@@ -617,12 +673,22 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const int p = member_of(tid, lane_lg_of(dz, a.h_lane, a.lane_lg, (int)U.n));
     const bool active = p < (int)U.n;
     const uint32_t id = d.st_first[s] + U.i0 + (uint32_t)p;
-    float fpsi[G], bpsi[G];
+    float fpsi[GP], bpsi[GP];
+#if !MOC_V2_PSI_SCALAR
+    if (active) {
+      load_q<GP>(a.psi_in, (int64_t)(2 * id), fpsi);
+      load_q<GP>(a.psi_in, (int64_t)(2 * id + 1), bpsi);
+    } else {
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      fpsi[g] = active ? a.psi_in[(size_t)(2 * id) * GP + g] : 0.f;
-      bpsi[g] = active ? a.psi_in[(size_t)(2 * id + 1) * GP + g] : 0.f;
+      for (int g = 0; g < GP; ++g) fpsi[g] = bpsi[g] = 0.f;
     }
+#else
+#pragma unroll
+    for (int g = 0; g < GP; ++g) {
+      fpsi[g] = active && g < G ? a.psi_in[(size_t)(2 * id) * GP + g] : 0.f;
+      bpsi[g] = active && g < G ? a.psi_in[(size_t)(2 * id + 1) * GP + g] : 0.f;
+    }
+#endif
     if (warp == 0) {
       int carry = 0;
       for (int b0 = 0; b0 < nk; b0 += 32) {
@@ -673,6 +739,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
       }
     }
     Physics<G, GP> ph;
+    ph.nem = 0u;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       float m = fmaxf(fpsi[g], bpsi[g]) * ps;
@@ -716,9 +783,17 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     }
 #pragma unroll 1
     for (int dir = 0; dir < 2; ++dir) {
+      {
+        float pin[GP] = {};  // re-read (an L1/L2 hit): holding both directions' psi costs spills
+#if !MOC_V2_PSI_SCALAR
+        if (active) load_q<GP>(a.psi_in, (int64_t)(2 * id + dir), pin);
+#else
 #pragma unroll
-      for (int g = 0; g < 2 * Physics<G, GP>::NP; ++g)
-        ph.psi(g) = active && g < G ? a.psi_in[(size_t)(2 * id + dir) * GP + g] * ps * ph.scl(g) : 0.f;
+        for (int g = 0; g < GP; ++g) pin[g] = active && g < G ? a.psi_in[(size_t)(2 * id + dir) * GP + g] : 0.f;
+#endif
+#pragma unroll
+        for (int g = 0; g < 2 * Physics<G, GP>::NP; ++g) ph.psi(g) = active && g < G ? pin[g] * ps * ph.scl(g) : 0.f;
+      }
       WalkState<G, GP> w;
       Replay<GP> r;
       if constexpr (otf) {
@@ -793,10 +868,18 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         int kc = x0 < x1 ? k_of_cell(base, k_lo, k_hi, cb + x0) : k_lo;
         for (int x = x0; x < x1; x += 32) {
           uint32_t* cp = cells + (size_t)x * (GP + 1);
+#if MOC_V2_NOCOUNT
+          constexpr uint32_t cnt = 0u;
+          uint32_t any = 0u;
+#pragma unroll
+          for (int g = 0; g < G; ++g) any |= cp[g];
+          if (!any) continue;
+#else
           const uint32_t cnt = cp[GP];
           if (!cnt) continue;
           cp[GP] = 0u;
           nemit += cnt;
+#endif
           while (base[kc + 1] <= cb + x) ++kc;
           const KSeg e = TF[kc];
           const int64_t j = (int64_t)(e.kx - e.ky) + cb + x;  // FSR of cell cb + x = ky + layer
@@ -824,8 +907,18 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
       if (active) {
         const uint32_t out = a.link[2 * id + dir];
         if (out != 0xffffffffu) {
+          if constexpr (GP == 8 && G < GP && !MOC_V2_PSI_SCALAR) {
+            // one 256-bit store of the whole slot (the pad word of psi is never read)
+            float v[8];
 #pragma unroll
-          for (int g = 0; g < G; ++g) a.psi_out[(size_t)out * GP + g] = ph.psi(g) * sh_iscale[g];
+            for (int g = 0; g < 8; ++g) v[g] = g < G ? ph.psi(g) * sh_iscale[g] : 0.f;
+            asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(a.psi_out + (size_t)out * GP),
+                         "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                         : "memory");
+          } else {
+#pragma unroll
+            for (int g = 0; g < G; ++g) a.psi_out[(size_t)out * GP + g] = ph.psi(g) * sh_iscale[g];
+          }
         } else {
           float e = 0.f;
 #pragma unroll
@@ -834,6 +927,9 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         }
       }
     }
+#if MOC_V2_NOCOUNT
+    nemit += ph.nem;
+#endif
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
