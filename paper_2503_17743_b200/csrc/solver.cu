@@ -17,6 +17,7 @@
 #include <thrust/sort.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -48,6 +49,7 @@ __constant__ float c_sigt[kMaxMat * kMaxG];      // sigma_t
 __constant__ float c_nusf[kMaxMat * kMaxG];
 __constant__ float c_chi[kMaxMat * kMaxG];
 __constant__ float c_sigs[kMaxMat * kMaxG * kMaxG];  // [m][from][to]
+__constant__ double c_planes[256];                   // axial planes (kMaxPlanes, sweep_v2.cuh)
 
 // device scalars (fp64): index map
 enum {
@@ -474,6 +476,8 @@ T* dmalloc(size_t n, int64_t& bytes) {
 struct moc_solver {
   std::string err;
   int device = 0;
+  uint64_t uid = 0;           // process-unique id: owner tag of the per-device __constant__ tables
+  double* h_planes = nullptr; // pinned copy of the axial planes (re-uploaded with the XS tables)
   cudaStream_t stream = nullptr;
   moc_solver_opts opts{};
   moc_comm_desc comm{0, 1, 0};
@@ -541,6 +545,28 @@ void upload(const void* h, void* d, size_t bytes, cudaStream_t st) {
   if (bytes) CUDA_OK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
 }
 
+// The __constant__ tables (cross sections, axial planes) are per device, shared by every
+// solver in the process: the solver whose kernels run next re-uploads its own copies when it
+// is not the last owner (one solver active per device at a time; stream-ordered uploads).
+uint64_t& const_owner(int dev) {
+  static uint64_t owner[64] = {};
+  return owner[dev & 63];
+}
+void ensure_constants(moc_solver* s) {
+  if (const_owner(s->device) == s->uid || !s->h_xs) return;
+  const size_t a = sizeof(float) * kMaxMat * kMaxG;
+  float* t2 = s->h_xs;
+  CUDA_OK(cudaMemcpyToSymbolAsync(c_sigt2, t2, a, 0, cudaMemcpyHostToDevice, s->stream));
+  CUDA_OK(cudaMemcpyToSymbolAsync(c_sigt, t2 + kMaxMat * kMaxG, a, 0, cudaMemcpyHostToDevice, s->stream));
+  CUDA_OK(cudaMemcpyToSymbolAsync(c_nusf, t2 + 2 * kMaxMat * kMaxG, a, 0, cudaMemcpyHostToDevice, s->stream));
+  CUDA_OK(cudaMemcpyToSymbolAsync(c_chi, t2 + 3 * kMaxMat * kMaxG, a, 0, cudaMemcpyHostToDevice, s->stream));
+  CUDA_OK(cudaMemcpyToSymbolAsync(c_sigs, t2 + 4 * kMaxMat * kMaxG, a * kMaxG, 0, cudaMemcpyHostToDevice, s->stream));
+  if (s->h_planes)
+    CUDA_OK(cudaMemcpyToSymbolAsync(c_planes, s->h_planes, sizeof(double) * (s->NL + 1), 0, cudaMemcpyHostToDevice,
+                                    s->stream));
+  const_owner(s->device) = s->uid;
+}
+
 // cross-section tables -> __constant__ (padded to kMaxMat x kMaxG); the fp32 tables the
 // kernels read; sigma_t * log2(e) for the ex2-based exponential.  Pinned staging buffer
 // so the copy is truly asynchronous on the solver's stream.
@@ -563,12 +589,9 @@ void upload_materials(moc_solver* s, const double* sigma_t, const double* sigma_
       for (int h = 0; h < G; ++h) ss[(m * kMaxG + q) * kMaxG + h] = (float)sigma_s[((size_t)m * G + q) * G + h];
     }
   const size_t a = sizeof(float) * kMaxMat * kMaxG;
-  CUDA_OK(cudaMemcpyToSymbolAsync(c_sigt2, t2, a, 0, cudaMemcpyHostToDevice, s->stream));
-  CUDA_OK(cudaMemcpyToSymbolAsync(c_sigt, t1, a, 0, cudaMemcpyHostToDevice, s->stream));
-  CUDA_OK(cudaMemcpyToSymbolAsync(c_nusf, nf, a, 0, cudaMemcpyHostToDevice, s->stream));
-  CUDA_OK(cudaMemcpyToSymbolAsync(c_chi, ch, a, 0, cudaMemcpyHostToDevice, s->stream));
-  CUDA_OK(cudaMemcpyToSymbolAsync(c_sigs, ss, a * kMaxG, 0, cudaMemcpyHostToDevice, s->stream));
   s->xs_bytes = (int64_t)(a * (4 + kMaxG));
+  const_owner(s->device) = 0;  // force the upload below
+  ensure_constants(s);
   s->sigma_t.assign(sigma_t, sigma_t + (size_t)NM * G);
   s->nusf.assign(nusf, nusf + (size_t)NM * G);
   s->sigs.assign(sigma_s, sigma_s + (size_t)NM * G * G);
@@ -649,6 +672,7 @@ void v2_configure(moc_solver* s) {
 // tally's tail so one all-reduce carries both.
 template <int G, int GP>
 void iter_sweep_half(moc_solver* s, bool time_it) {
+  ensure_constants(s);
   const bool v2 = s->opts.schedule == 0;
   const int nb = s->nb_fsr;
   k_source<G, GP><<<nb, 256, 0, s->stream>>>(s->J, s->d_mat, s->d_phi, s->d_vol, s->d_sc, s->d_qt, s->d_fold,
@@ -678,6 +702,7 @@ void iter_sweep_half(moc_solver* s, bool time_it) {
 // second half: (after the caller's all-reduce / halo exchange) scatter the halo, A7.
 template <int G, int GP>
 void iter_finish_half(moc_solver* s) {
+  ensure_constants(s);
   const bool v2 = s->opts.schedule == 0;
   const int nb = s->nb_fsr;
   if (s->comm.world > 1) {
@@ -784,6 +809,8 @@ void destroy(moc_solver* s) {
   for (auto& e : s->ev)
     if (e) cudaEventDestroy(e);
   if (s->h_xs) cudaFreeHost(s->h_xs);
+  if (s->h_planes) cudaFreeHost(s->h_planes);
+  if (const_owner(s->device) == s->uid) const_owner(s->device) = 0;
 }
 
 }  // namespace
@@ -825,6 +852,8 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     if (opts) s->opts = *opts;
     if (comm) s->comm = *comm;
     s->device = device;
+    static std::atomic<uint64_t> next_uid{1};
+    s->uid = next_uid++;
     CUDA_OK(cudaSetDevice(device));
     s->stream = (cudaStream_t)cuda_stream;
     s->G = mt.G;
@@ -859,6 +888,10 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     upload(L.seg_send.data(), s->d_seg_send, 8 * s->N2, st);
     upload(L.seg_region.data(), s->d_seg_region, 4 * s->N2, st);
     upload(g.planes.data(), s->d_planes, 8 * (g.NL + 1), st);
+    if (g.NL + 1 <= 256) {
+      CUDA_OK(cudaMallocHost(&s->h_planes, sizeof(double) * (g.NL + 1)));
+      std::memcpy(s->h_planes, g.planes.data(), sizeof(double) * (g.NL + 1));
+    }
     upload(L.t_len.data(), s->d_t_len, 8 * s->T2, st);
     upload(L.t_seg.data(), s->d_t_seg, 8 * (s->T2 + 1), st);
     upload(L.t_a.data(), s->d_t_a, 4 * s->T2, st);
@@ -983,7 +1016,7 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       // the tile left below the largest unit's tables must hold two full layer columns
       s->cap_cells = (int)std::min<int64_t>(
           cap_max_cells(s->GP),
-          (((int64_t)s->v2_smem - unit_table_bytes((int)max_nk)) / (4 * (s->GP + 1))) & ~7);
+          (((int64_t)s->v2_smem - unit_table_bytes((int)max_nk)) / cell_bytes(s->GP)) & ~7);
       s->tile_off = (unit_table_bytes((int)max_nk) + 15) & ~15;
       if (s->cap_cells < 2 * g.NL) throw Error(MOC_E_CAPACITY, "axial mesh too fine for the tally tile");
       if (s->opts.tile_cells > 0) {

@@ -54,6 +54,13 @@ constexpr uint64_t kNoExp = ~0ull;
 #ifndef MOC_V2_NOCOUNT
 #define MOC_V2_NOCOUNT 1
 #endif
+#ifndef MOC_V2_SIG_CONST
+#define MOC_V2_SIG_CONST 1
+#endif
+#ifndef MOC_V2_PLANES_CONST
+#define MOC_V2_PLANES_CONST 0
+#endif
+static_assert(kMaxPlanes == sizeof(c_planes) / sizeof(double), "c_planes sized for kMaxPlanes");
 #ifndef MOC_V2_PSI_SCALAR
 #define MOC_V2_PSI_SCALAR 0  // 1: per-group 32-bit boundary-psi loads / stores (A/B)
 #endif            // unit not preloaded (on-the-fly)
@@ -84,7 +91,14 @@ struct __align__(16) KSeg {
 // in different cells on different banks).  The tile never moves and stays zero between
 // flushes.
 __host__ __device__ constexpr int unit_table_bytes(int nk) { return 32 * nk + ((8 * (nk + 1) + 15) & ~15); }
-__host__ __device__ constexpr int cap_max_cells(int GP) { return (56000 / (4 * GP + 4)) & ~7; }
+#ifndef MOC_V2_TILE_COPIES
+#define MOC_V2_TILE_COPIES 1
+#endif
+// copies of the tile: lane parity picks the copy, so neighbouring lanes in one cell (the
+// common same-address atomic conflict) hit different words; the flush sums the copies
+constexpr int kTileCopies = MOC_V2_TILE_COPIES;
+__host__ __device__ constexpr int cell_bytes(int GP) { return 4 * (GP + 1) * kTileCopies; }
+__host__ __device__ constexpr int cap_max_cells(int GP) { return (56000 / cell_bytes(GP)) & ~7; }
 
 struct Unit {
   uint32_t stack, i0, n, cost;
@@ -231,9 +245,12 @@ struct Physics {
   uint32_t psa;  // shared address of sh_planes
   uint32_t nem;  // emissions (MOC_V2_NOCOUNT: the tile has no per-cell count)
 
-  // axial plane i (an LDS.64 from the register-held base)
+  // axial plane i: from the constant bank (MOC_V2_PLANES_CONST; off the L1 data pipe) or an
+  // LDS.64 from the register-held shared base
   __device__ __forceinline__ double plane(int i) const {
-#ifndef MOC_V2_GENERIC_SMEM
+#if MOC_V2_PLANES_CONST
+    return c_planes[i];
+#elif !defined(MOC_V2_GENERIC_SMEM)
     double z;
     asm("ld.shared.f64 %0, [%1];" : "=d"(z) : "r"(psa + 8u * (uint32_t)i));
     return z;
@@ -265,7 +282,12 @@ struct Physics {
     asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(ca), "n"(4 * GP));
 #endif
     float sg[GP];
-    if constexpr (GP % 4 == 0) {
+    if constexpr (MOC_V2_SIG_CONST) {
+      // Sigma_t from the constant bank (LDC through the constant cache, off the L1 data pipe;
+      // lanes mostly share the material, else the load replays per distinct address)
+#pragma unroll
+      for (int h = 0; h < GP; ++h) sg[h] = h < G ? c_sigt2[m * kMaxG + h] : 0.f;
+    } else if constexpr (GP % 4 == 0) {
 #pragma unroll
       for (int h = 0; h < GP / 4; ++h)
         asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -621,7 +643,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
   }
   for (int q = tid; q <= d.NL; q += blockDim.x) sh_planes[q] = d.planes[q];
   // the tile starts zeroed; each flush re-zeroes exactly the cells it consumed
-  for (int q = tid; q < cap * (GP + 1); q += blockDim.x) cells[q] = 0u;
+  for (int q = tid; q < cap * (GP + 1) * kTileCopies; q += blockDim.x) cells[q] = 0u;
   const float ps = (float)a.sc[SC_PSI_SCALE];
   const OtfView v{nullptr, nullptr, sh_planes, d.NL};
   double leak = 0.0;
@@ -843,7 +865,8 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const int k_lo = chunk[c], k_hi = chunk[c + 1];
         const int cb = base[k_lo], ce = base[k_hi];
         ph.cb = cb;
-        ph.tsa = opaque_u32(tile_sa - (uint32_t)cb * (4u * (GP + 1)));
+        ph.tsa = opaque_u32(tile_sa - (uint32_t)cb * (4u * (GP + 1)) +
+                            (uint32_t)((lane % kTileCopies) * cap) * (4u * (GP + 1)));
 #ifdef MOC_DEBUG_WALK
         ph.dbg_lo = cb;
         ph.dbg_hi = ce;
@@ -871,8 +894,14 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
 #if MOC_V2_NOCOUNT
           constexpr uint32_t cnt = 0u;
           uint32_t any = 0u;
+          uint32_t sum[GP];
 #pragma unroll
-          for (int g = 0; g < G; ++g) any |= cp[g];
+          for (int g = 0; g < G; ++g) {
+            sum[g] = cp[g];
+#pragma unroll
+            for (int c = 1; c < kTileCopies; ++c) sum[g] += cp[(size_t)c * cap * (GP + 1) + g];
+            any |= sum[g];
+          }
           if (!any) continue;
 #else
           const uint32_t cnt = cp[GP];
@@ -886,8 +915,15 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
           uint32_t raw[GP];
 #pragma unroll
           for (int g = 0; g < GP; ++g) {
+#if MOC_V2_NOCOUNT
+            raw[g] = g < G ? sum[g] : 0u;  // pad words are never written
+            if (g < G)
+#pragma unroll
+              for (int c = 0; c < kTileCopies; ++c) cp[(size_t)c * cap * (GP + 1) + g] = 0u;
+#else
             raw[g] = g < G ? cp[g] : kMagicBits * cnt;  // pad words are never written
             if (g < G) cp[g] = 0u;
+#endif
           }
           float val[GP];
 #pragma unroll

@@ -201,3 +201,24 @@ def test_cfg3_reduced_fixed_iterations(M, oracle_mod):
     assert k == pytest.approx(ref["k"], abs=1e-5)
     linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
     assert linf < 1e-4, (linf, rel)
+
+
+def test_interleaved_solvers_keep_their_constants(M):
+    """Two live solvers on one device with different cross sections and axial meshes: the
+    per-device __constant__ tables (XS, planes) follow the solver whose kernels run, so
+    interleaved iterations give the same k and flux as each solver run alone."""
+    pa, pb = P.small_lattice(3, 3, 4), P.config(2)
+    alone = []
+    for prob in (pa, pb):
+        s = M.Solver(M.Problem(prob))
+        k, _ = s.iterate(4)
+        alone.append((k, s.scalar_flux()))
+        del s
+    sa, sb = M.Solver(M.Problem(pa)), M.Solver(M.Problem(pb))
+    for _ in range(4):
+        ka, _ = sa.iterate(1)
+        kb, _ = sb.iterate(1)
+    # equal up to the order of the fp32 global tally reductions
+    assert ka == pytest.approx(alone[0][0], abs=1e-6) and kb == pytest.approx(alone[1][0], abs=1e-6)
+    for s, (_, ref) in ((sa, alone[0]), (sb, alone[1])):
+        assert np.abs(s.scalar_flux() - ref).max() / np.abs(ref).max() < 1e-5
