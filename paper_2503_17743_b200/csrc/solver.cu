@@ -522,6 +522,7 @@ struct moc_solver {
   float *d_rmax = nullptr, *d_qmax_t = nullptr, *d_tally32 = nullptr;
   int* d_err = nullptr;
   int cap_cells = 0;  // v2 tile capacity in cells (sweep_v2.cuh layout)
+  int interleave = 1; // v2 sibling units interleaved per member range (Unit::step)
   int tile_off = 0;   // v2 tile byte offset (above the largest unit's tables)
   int lane_lg = -1;  // forced log2 v2 lane stride (MOC_V2_LANE_STRIDE), -1 = per unit
   double h_lane = 0;     // thinnest axial layer / 3 (sweep_v2.cuh lane_lg_of)
@@ -1028,6 +1029,7 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
         for (int l = 0; l < g.NL; ++l) hmin = std::min(hmin, g.planes[l + 1] - g.planes[l]);
         const char* dv = std::getenv("MOC_V2_LANE_DIV");  // A/B override of the 1/3
         s->h_lane = hmin / (dv ? std::atof(dv) : 3.0);
+        if (const char* e = std::getenv("MOC_V2_INTERLEAVE")) s->interleave = std::max(1, std::min(8, std::atoi(e)));
         if (const char* e = std::getenv("MOC_V2_LANE_STRIDE")) {  // A/B override
           const int v = std::atoi(e);
           s->lane_lg = v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0;
@@ -1037,8 +1039,14 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       for (int64_t q = 0; q < s->S; ++q) {
         if (!owner.empty() && owner[q] != s->comm.rank) continue;
         const int64_t cnt = L.st_cnt[q];
-        for (int64_t i0 = 0; i0 < cnt; i0 += kV2Threads)
-          units.push_back(Unit{(uint32_t)q, (uint32_t)i0, (uint32_t)std::min<int64_t>(kV2Threads, cnt - i0), 0u});
+        // R sibling units interleave over each range of R * kV2Threads members (lanes of a
+        // warp then sit R times further apart in z: fewer same-cell shared atomics)
+        const int64_t R = s->interleave;
+        for (int64_t b0 = 0; b0 < cnt; b0 += R * kV2Threads) {
+          const int64_t blk = std::min<int64_t>(R * kV2Threads, cnt - b0);
+          for (int64_t r = 0; r < R && r < blk; ++r)
+            units.push_back(Unit{(uint32_t)q, (uint32_t)(b0 + r), (uint32_t)((blk - r + R - 1) / R), (uint32_t)R});
+        }
       }
       s->n_units = (uint32_t)units.size();
       s->d_units = dmalloc<Unit>(units.size(), B);

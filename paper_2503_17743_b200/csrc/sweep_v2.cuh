@@ -100,8 +100,10 @@ constexpr int kTileCopies = MOC_V2_TILE_COPIES;
 __host__ __device__ constexpr int cell_bytes(int GP) { return 4 * (GP + 1) * kTileCopies; }
 __host__ __device__ constexpr int cap_max_cells(int GP) { return (56000 / cell_bytes(GP)) & ~7; }
 
+// members i0, i0 + step, ..., i0 + (n - 1) step of one z-stack (step > 1 interleaves
+// sibling units over one range, spreading a warp's lanes further apart in z)
 struct Unit {
-  uint32_t stack, i0, n, cost;
+  uint32_t stack, i0, n, step;
 };
 
 // merged segment record: meta = kk | layer << 10 | material << 18, plus the 3D length
@@ -664,7 +666,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const int nk = (int)(d.t_seg[t + 1] - sb);
     const double dz = d.an_dz[an], cot = d.an_cot[an];
     const double z0b = d.st_z0[s];
-    const double zf = z0b + (double)U.i0 * dz, zl = z0b + (double)(U.i0 + U.n - 1) * dz;
+    const double zf = z0b + (double)U.i0 * dz, zl = z0b + (double)(U.i0 + (U.n - 1) * U.step) * dz;
     // per-unit tables at the top of the dynamic buffer, the tile below them
     KSeg* const TF = reinterpret_cast<KSeg*>(dsm);
     KSeg* const TB = TF + nk;
@@ -692,9 +694,9 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     __syncthreads();
     // 3. one track per thread (member_of: neighbouring members share a warp); its incoming
     //    psi loads are issued here so their HBM latency overlaps the scan below
-    const int p = member_of(tid, lane_lg_of(dz, a.h_lane, a.lane_lg, (int)U.n));
+    const int p = member_of(tid, lane_lg_of(dz * U.step, a.h_lane, a.lane_lg, (int)U.n));
     const bool active = p < (int)U.n;
-    const uint32_t id = d.st_first[s] + U.i0 + (uint32_t)p;
+    const uint32_t id = d.st_first[s] + U.i0 + (uint32_t)p * U.step;
     float fpsi[GP], bpsi[GP];
 #if !MOC_V2_PSI_SCALAR
     if (active) {
@@ -786,7 +788,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     ph.ssa = opaque_u32((uint32_t)__cvta_generic_to_shared(sh_sig));
     ph.psa = opaque_u32((uint32_t)__cvta_generic_to_shared(sh_planes));
     const double tn = d.an_tan[an], isn = d.an_invsin[an], Lt = d.t_len[t];
-    const double z0 = z0b + (double)(U.i0 + p) * dz;
+    const double z0 = z0b + (double)(U.i0 + (uint32_t)p * U.step) * dz;
     const bool up = cot > 0;
     const float cw = d.an_c[an];
     constexpr bool otf = !EXP;
@@ -985,10 +987,11 @@ __global__ void k_exp_generate(DevData d, const Unit* units, const uint64_t* uni
   for (uint32_t u = blockIdx.x; u < n_units; u += gridDim.x) {
     if (unit_exp[u] == kNoExp) continue;
     const Unit U = units[u];
-    const int p = member_of(threadIdx.x, lane_lg_of(d.an_dz[d.t_a[U.stack / d.N] * d.N + U.stack % d.N], h_lane, lane_lg, (int)U.n));
+    const int p = member_of(threadIdx.x, lane_lg_of(d.an_dz[d.t_a[U.stack / d.N] * d.N + U.stack % d.N] * U.step,
+                                                    h_lane, lane_lg, (int)U.n));
     if (p >= (int)U.n) continue;
     int s, an;
-    const uint32_t id = d.st_first[U.stack] + U.i0 + (uint32_t)p;
+    const uint32_t id = d.st_first[U.stack] + U.i0 + (uint32_t)p * U.step;
     TrackGeo g = dev_track(d, id, s, an);
     Rec* rs = store + unit_exp[u] + threadIdx.x;
     int q = 0;
@@ -1043,8 +1046,8 @@ __global__ void k_unit_cost(const Unit* units, uint32_t n_units, const uint32_t*
     const uint32_t f = st_first[U.stack] + U.i0;
     uint32_t c = 0, mx = 0;
     for (uint32_t i = 0; i < U.n; ++i) {
-      c += cost[f + i];
-      mx = max(mx, cost[f + i]);
+      c += cost[f + i * U.step];
+      mx = max(mx, cost[f + i * U.step]);
     }
     key[u] = c;
     maxq[u] = mx;
