@@ -617,6 +617,7 @@ void run_sweep(moc_solver* s) {
     a.sc = s->d_sc;
     a.tile_off = s->tile_off;
     a.cap_cells = s->cap_cells;
+    a.stage_off = s->tile_off + s->cap_cells * cell_bytes(s->GP);  // staged sources follow the tile
     a.lane_lg = s->lane_lg;
     a.h_lane = s->h_lane;
     a.err = s->d_err;
@@ -1016,8 +1017,8 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       v2_configure_any(s);  // dynamic shared memory from the kernel's static footprint
       // the tile left below the largest unit's tables must hold two full layer columns
       s->cap_cells = (int)std::min<int64_t>(
-          cap_max_cells(s->GP),
-          (((int64_t)s->v2_smem - unit_table_bytes((int)max_nk)) / cell_bytes(s->GP)) & ~7);
+          cap_max_cells(s->G, s->GP),
+          (((int64_t)s->v2_smem - unit_table_bytes((int)max_nk)) / cell_bytes(s->G, s->GP)) & ~7);
       s->tile_off = (unit_table_bytes((int)max_nk) + 15) & ~15;
       if (s->cap_cells < 2 * g.NL) throw Error(MOC_E_CAPACITY, "axial mesh too fine for the tally tile");
       if (s->opts.tile_cells > 0) {

@@ -97,8 +97,21 @@ __host__ __device__ constexpr int unit_table_bytes(int nk) { return 32 * nk + ((
 // copies of the tile: lane parity picks the copy, so neighbouring lanes in one cell (the
 // common same-address atomic conflict) hit different words; the flush sums the copies
 constexpr int kTileCopies = MOC_V2_TILE_COPIES;
+#ifndef MOC_V2_QSTAGE
+#define MOC_V2_QSTAGE 0
+#endif
+// MOC_V2_QSTAGE: each chunk's FSR sources (and material, in the pad slot) are staged in
+// shared memory next to the tile, one coalesced pass per chunk, and Eq. 3 reads them with
+// two LDS.128 instead of one scattered 256-bit global load per segment (each distinct FSR
+// record a lane touches costs an L1 data-pipe wavefront).  Needs the pad slot (G < GP).
+// Measured slower (cfg4 20.4 vs 17.2 ms, cfg5 130.3 vs 126.2 ms): the staged LDS.128 pair
+// costs as many data-pipe wavefronts as the global load it replaces (bank conflicts between
+// lanes' 32-byte records; ncu shared-load wavefronts 3.8e9 -> 15.6e9 on cfg5) and the
+// halved tile capacity doubles the chunk steps.
+__host__ __device__ constexpr bool staged(int G, int GP) { return MOC_V2_QSTAGE && G < GP; }
 __host__ __device__ constexpr int cell_bytes(int GP) { return 4 * (GP + 1) * kTileCopies; }
-__host__ __device__ constexpr int cap_max_cells(int GP) { return (56000 / cell_bytes(GP)) & ~7; }
+__host__ __device__ constexpr int cell_bytes(int G, int GP) { return cell_bytes(GP) + (staged(G, GP) ? 4 * GP : 0); }
+__host__ __device__ constexpr int cap_max_cells(int G, int GP) { return (56000 / cell_bytes(G, GP)) & ~7; }
 
 // members i0, i0 + step, ..., i0 + (n - 1) step of one z-stack (step > 1 interleaves
 // sibling units over one range, spreading a warp's lanes further apart in z)
@@ -132,6 +145,7 @@ struct V2Args {
   const Rec* store;     // EXP record store
   const uint32_t* cost; // exact merged segments per track (EXP replay length)
   int tile_off;         // byte offset of the tile in the dynamic buffer (multiple of 16)
+  int stage_off;        // byte offset of the staged sources [cap][GP] f32 (MOC_V2_QSTAGE)
   int cap_cells;        // tile capacity in cells (multiple of 8)
   double h_lane;        // thinnest axial layer / 3 (lane_lg_of)
   int lane_lg;          // forced log2 lane stride, -1 = per unit (lane_lg_of)
@@ -246,6 +260,20 @@ struct Physics {
   uint32_t ssa;  // shared address of sh_sig
   uint32_t psa;  // shared address of sh_planes
   uint32_t nem;  // emissions (MOC_V2_NOCOUNT: the tile has no per-cell count)
+  uint32_t qsa;  // shared address of the staged sources minus cb records
+  static constexpr bool kStaged = staged(G, GP);
+
+  // Eq. 3 for pending cell pc with its source and material read from the chunk's stage
+  __device__ __forceinline__ void emit_staged(int pc, float Lf) {
+    float q[GP];
+    const uint32_t qa = qsa + (uint32_t)pc * (4u * GP);
+#pragma unroll
+    for (int h = 0; h < GP / 4; ++h)
+      asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+          : "=f"(q[4 * h]), "=f"(q[4 * h + 1]), "=f"(q[4 * h + 2]), "=f"(q[4 * h + 3])
+          : "r"(qa + 16u * h));
+    emit(pc, __float_as_int(q[G]), q, Lf);
+  }
 
   // axial plane i: from the constant bank (MOC_V2_PLANES_CONST; off the L1 data pipe) or an
   // LDS.64 from the register-held shared base
@@ -380,13 +408,21 @@ struct WalkState {
     kx = v.z;
     ky = v.w;
   }
-  // make raw piece (k, l) the pending segment: its cell, source and material
+  // make raw piece (k, l) the pending segment: its cell, source and material (staged:
+  // only the cell; Eq. 3 reads the chunk's stage)
   __device__ __forceinline__ void set_pending(int jx, int cy, int ll, const uint8_t* mat, const float* qt) {
-    const int64_t j = (int64_t)(jx + ll);
     pc = cy + ll;
-    load_q<GP>(qt, j, pq);
-    if constexpr (G < GP) pm = __float_as_int(pq[G]);  // material index rides in the pad slot
-    else pm = mat[j];
+    if constexpr (!staged(G, GP)) {
+      const int64_t j = (int64_t)(jx + ll);
+      load_q<GP>(qt, j, pq);
+      if constexpr (G < GP) pm = __float_as_int(pq[G]);  // material index rides in the pad slot
+      else pm = mat[j];
+    }
+  }
+  template <class PH>
+  __device__ __forceinline__ void emit_to(PH& ph, float L) {
+    if constexpr (staged(G, GP)) ph.emit_staged(pc, L);
+    else ph.emit(pc, pm, pq, L);
   }
 };
 
@@ -399,14 +435,14 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
     if (w.pc >= c_hi) return;
     if (w.done) {
       if (w.pc >= 0) {
-        ph.emit(w.pc, w.pm, w.pq, w.pL);
+        w.emit_to(ph, w.pL);
         w.pc = -1;
         w.fkl = -1;  // the track is finished: no all-sliver emission follows
       } else if (w.fkl >= 0) {  // all-sliver track: one segment at its first piece
         const KSeg e = TF[w.fkl & 0xffff];
         if (e.ky + (w.fkl >> 16) >= c_hi) return;
         w.set_pending(e.kx, e.ky, w.fkl >> 16, ph.mat, ph.qt);
-        ph.emit(w.pc, w.pm, w.pq, w.carry);
+        w.emit_to(ph, w.carry);
         w.pc = -1;
         w.fkl = -1;
       }
@@ -433,7 +469,7 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
         if (w.fkl < 0) w.fkl = w.k | (w.l << 16);
       }
     } else {
-      if (w.pc >= 0) ph.emit(w.pc, w.pm, w.pq, w.pL);
+      if (w.pc >= 0) w.emit_to(ph, w.pL);
       w.pL = L3 + w.carry;
       w.carry = 0.f;
       w.set_pending(w.kx, w.ky, w.l, ph.mat, ph.qt);
@@ -480,14 +516,14 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, G
     if ((unsigned)w.pc < (unsigned)c_lo) return;
     if (w.done) {
       if (w.pc >= 0) {
-        ph.emit(w.pc, w.pm, w.pq, w.pL + w.carry);
+        w.emit_to(ph, w.pL + w.carry);
         w.pc = -1;
         w.fkl = -1;  // the track is finished: no all-sliver emission follows
       } else if (w.fkl >= 0) {  // all-sliver track: emitted in the chunk of its first piece
         const KSeg e = TF[w.fkl & 0xffff];
         if (e.ky + (w.fkl >> 16) < c_lo) return;
         w.set_pending(e.kx, e.ky, w.fkl >> 16, ph.mat, ph.qt);
-        ph.emit(w.pc, w.pm, w.pq, w.carry);
+        w.emit_to(ph, w.carry);
         w.pc = -1;
         w.fkl = -1;
       }
@@ -507,7 +543,7 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, G
       w.carry += L3;
       if (w.pc < 0) w.fkl = w.k | (w.l << 16);  // the forward-first sliver wins
     } else {
-      if (w.pc >= 0) ph.emit(w.pc, w.pm, w.pq, w.pL);
+      if (w.pc >= 0) w.emit_to(ph, w.pL);
       w.pL = L3 + w.carry;
       w.carry = 0.f;
       w.set_pending(w.kx, w.ky, w.l, ph.mat, ph.qt);
@@ -623,6 +659,27 @@ __device__ __forceinline__ int k_of_cell(const int* base, int k_lo, int k_hi, in
     if (base[mid] <= c) lo = mid; else hi = mid - 1;
   }
   return lo;
+}
+
+// Stage chunk [k_lo, k_hi)'s FSR records (source + material) into stage[0, ce - cb): each
+// warp a contiguous share of the cells, lane-strided (consecutive cells of one 2D segment
+// are consecutive FSRs, so the global reads coalesce), cell -> 2D segment as in the flush.
+template <int GP>
+__device__ __forceinline__ void stage_chunk(float* stage, const float* qt, const KSeg* TF, const int* base, int k_lo,
+                                            int k_hi, int warp, int lane, int nw) {
+  const int cb = base[k_lo], n = base[k_hi] - cb;
+  const int per = (n + nw - 1) / nw;
+  const int x0 = warp * per + lane, x1 = min(n, (warp + 1) * per);
+  int kc = x0 < x1 ? k_of_cell(base, k_lo, k_hi, cb + x0) : k_lo;
+  for (int x = x0; x < x1; x += 32) {
+    while (base[kc + 1] <= cb + x) ++kc;
+    const KSeg e = TF[kc];
+    float v[GP];
+    load_q<GP>(qt, (int64_t)(e.kx - e.ky) + cb + x, v);
+#pragma unroll
+    for (int h = 0; h < GP / 4; ++h)
+      reinterpret_cast<float4*>(stage + (size_t)x * GP)[h] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+  }
 }
 
 // EXP = false: on-the-fly sweep of the units past the preloaded prefix (the replay path
@@ -772,6 +829,9 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
       if (lane == 0) atomicMax(&sh_max[g], __float_as_uint(m));
     }
     __syncthreads();
+    constexpr bool kStage = Physics<G, GP>::kStaged && !EXP;
+    float* const stage = reinterpret_cast<float*>(dsm + a.stage_off);  // [cap][GP] (kStage)
+    if constexpr (kStage) stage_chunk<GP>(stage, a.qt, TF, base, chunk[0], chunk[1], warp, lane, nw);
     if (tid < G) {
       const float b = fmaxf(__uint_as_float(sh_max[tid]), a.qmax_t[(size_t)t * GP + tid]) * 1.0001f;
       sh_scale[tid] = b > 0.f ? kFixOne / b : 0.f;
@@ -785,6 +845,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     ph.qt = a.qt;
     ph.tile_off = a.tile_off;
     const uint32_t tile_sa = (uint32_t)__cvta_generic_to_shared(dsm) + (uint32_t)a.tile_off;
+    const uint32_t stage_sa = (uint32_t)__cvta_generic_to_shared(dsm) + (uint32_t)a.stage_off;
     ph.ssa = opaque_u32((uint32_t)__cvta_generic_to_shared(sh_sig));
     ph.psa = opaque_u32((uint32_t)__cvta_generic_to_shared(sh_planes));
     const double tn = d.an_tan[an], isn = d.an_invsin[an], Lt = d.t_len[t];
@@ -869,6 +930,8 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         ph.cb = cb;
         ph.tsa = opaque_u32(tile_sa - (uint32_t)cb * (4u * (GP + 1)) +
                             (uint32_t)((lane % kTileCopies) * cap) * (4u * (GP + 1)));
+        // the stage holds this chunk (staged at the unit start or by the previous flush phase)
+        if constexpr (kStage) ph.qsa = opaque_u32(stage_sa - (uint32_t)cb * (4u * GP));
 #ifdef MOC_DEBUG_WALK
         ph.dbg_lo = cb;
         ph.dbg_hi = ce;
@@ -939,6 +1002,11 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
 #pragma unroll
             for (int g = 0; g < G; ++g) atomicAdd(dst + g, val[g]);
           }
+        }
+        // stage the chunk walked next (forward: c + 1; backward: c - 1) in the same phase
+        if constexpr (kStage) {
+          const int cn = dir == 0 ? c + 1 : (ci + 1 < nchunk ? c - 1 : -1);
+          if (cn >= 0) stage_chunk<GP>(stage, a.qt, TF, base, chunk[cn], chunk[cn + 1], warp, lane, nw);
         }
         __syncthreads();
       }
