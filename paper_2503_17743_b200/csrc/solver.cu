@@ -617,7 +617,7 @@ void run_sweep(moc_solver* s) {
     a.sc = s->d_sc;
     a.tile_off = s->tile_off;
     a.cap_cells = s->cap_cells;
-    a.stage_off = s->tile_off + s->cap_cells * cell_bytes(s->GP);  // staged sources follow the tile
+    a.stage_off = s->tile_off + s->cap_cells * tile_cell_bytes(s->G, s->GP);  // staged sources follow the tile
     a.lane_lg = s->lane_lg;
     a.h_lane = s->h_lane;
     a.err = s->d_err;

@@ -86,7 +86,7 @@ struct __align__(16) KSeg {
 
 // Dynamic shared memory of one CTA: the per-unit tables from the bottom (TF[nk] at offset
 // 0, so a radial step's address is one shift from the buffer base | TB[nk] | base[nk+1] |
-// chunk[nk+1]), then the tile [cap][GP + 1] u32 at a per-solver offset (tile_off >= the
+// chunk[nk+1]), then the tile [cap][cell_words] u32 at a per-solver offset (tile_off >= the
 // largest unit's tables; GP group words + the segment count, the odd stride keeping lanes
 // in different cells on different banks).  The tile never moves and stays zero between
 // flushes.
@@ -109,8 +109,16 @@ constexpr int kTileCopies = MOC_V2_TILE_COPIES;
 // lanes' 32-byte records; ncu shared-load wavefronts 3.8e9 -> 15.6e9 on cfg5) and the
 // halved tile capacity doubles the chunk steps.
 __host__ __device__ constexpr bool staged(int G, int GP) { return MOC_V2_QSTAGE && G < GP; }
-__host__ __device__ constexpr int cell_bytes(int GP) { return 4 * (GP + 1) * kTileCopies; }
-__host__ __device__ constexpr int cell_bytes(int G, int GP) { return cell_bytes(GP) + (staged(G, GP) ? 4 * GP : 0); }
+// tile cell stride in u32 words: the G group words (plus the count word without
+// MOC_V2_NOCOUNT), rounded up to an odd count so lanes in consecutive cells hit distinct banks
+#ifndef MOC_V2_CELL_GP1
+#define MOC_V2_CELL_GP1 0  // 1: stride GP + 1 words as before the offset-free codes (A/B)
+#endif
+__host__ __device__ constexpr int cell_words(int G, int GP) {
+  return MOC_V2_NOCOUNT && !MOC_V2_CELL_GP1 ? (G | 1) : GP + 1;
+}
+__host__ __device__ constexpr int tile_cell_bytes(int G, int GP) { return 4 * cell_words(G, GP) * kTileCopies; }
+__host__ __device__ constexpr int cell_bytes(int G, int GP) { return tile_cell_bytes(G, GP) + (staged(G, GP) ? 4 * GP : 0); }
 __host__ __device__ constexpr int cap_max_cells(int G, int GP) { return (56000 / cell_bytes(G, GP)) & ~7; }
 
 // members i0, i0 + step, ..., i0 + (n - 1) step of one z-stack (step > 1 interleaves
@@ -256,7 +264,7 @@ struct Physics {
   const float* qt;
   int cb;        // first cell of the current chunk (tile cell 0)
   int tile_off;  // byte offset of the tile in the dynamic buffer
-  uint32_t tsa;  // shared address of the tile minus cb cells (cell pc at tsa + pc * 4 (GP + 1))
+  uint32_t tsa;  // shared address of the tile minus cb cells (cell pc at tsa + pc * 4 cell_words)
   uint32_t ssa;  // shared address of sh_sig
   uint32_t psa;  // shared address of sh_planes
   uint32_t nem;  // emissions (MOC_V2_NOCOUNT: the tile has no per-cell count)
@@ -307,7 +315,7 @@ struct Physics {
     // 32-bit shared-window addresses held in registers (tile base pre-offset by the
     // chunk's first cell; Sigma_t table base): one IMAD / LEA per emit instead of the
     // compiler re-deriving both generic->shared bases (S2UR CgaCtaId, ULEA, LDC) each time
-    const uint32_t ca = tsa + (uint32_t)pc * (4u * (GP + 1));
+    const uint32_t ca = tsa + (uint32_t)pc * (4u * cell_words(G, GP));
 #if !MOC_V2_NOCOUNT
     asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(ca), "n"(4 * GP));
 #endif
@@ -337,7 +345,7 @@ struct Physics {
 #else
     extern __shared__ __align__(16) uint8_t dsm[];
     const int x = pc - cb;
-    uint32_t* cell = reinterpret_cast<uint32_t*>(dsm + tile_off) + x * (GP + 1);
+    uint32_t* cell = reinterpret_cast<uint32_t*>(dsm + tile_off) + x * cell_words(G, GP);
     atomicAdd(cell + GP, 1u);
     float sg[GP];
     if constexpr (GP % 4 == 0) {
@@ -689,7 +697,8 @@ template <int G, int GP, bool EXP>
 __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a) {
   extern __shared__ __align__(16) uint8_t dsm[];
   const int cap = a.cap_cells;
-  uint32_t* const cells = reinterpret_cast<uint32_t*>(dsm + a.tile_off);  // [cap][GP + 1]
+  uint32_t* const cells = reinterpret_cast<uint32_t*>(dsm + a.tile_off);  // [cap][kCW]
+  constexpr int kCW = cell_words(G, GP);
   __shared__ uint32_t s_unit;
   __shared__ int s_nchunk;
 
@@ -702,7 +711,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
   }
   for (int q = tid; q <= d.NL; q += blockDim.x) sh_planes[q] = d.planes[q];
   // the tile starts zeroed; each flush re-zeroes exactly the cells it consumed
-  for (int q = tid; q < cap * (GP + 1) * kTileCopies; q += blockDim.x) cells[q] = 0u;
+  for (int q = tid; q < cap * kCW * kTileCopies; q += blockDim.x) cells[q] = 0u;
   const float ps = (float)a.sc[SC_PSI_SCALE];
   const OtfView v{nullptr, nullptr, sh_planes, d.NL};
   double leak = 0.0;
@@ -928,8 +937,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const int k_lo = chunk[c], k_hi = chunk[c + 1];
         const int cb = base[k_lo], ce = base[k_hi];
         ph.cb = cb;
-        ph.tsa = opaque_u32(tile_sa - (uint32_t)cb * (4u * (GP + 1)) +
-                            (uint32_t)((lane % kTileCopies) * cap) * (4u * (GP + 1)));
+        ph.tsa = opaque_u32(tile_sa - (uint32_t)cb * (4u * kCW) + (uint32_t)((lane % kTileCopies) * cap) * (4u * kCW));
         // the stage holds this chunk (staged at the unit start or by the previous flush phase)
         if constexpr (kStage) ph.qsa = opaque_u32(stage_sa - (uint32_t)cb * (4u * GP));
 #ifdef MOC_DEBUG_WALK
@@ -955,7 +963,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const int x0 = warp * per + lane, x1 = min(ce - cb, (warp + 1) * per);
         int kc = x0 < x1 ? k_of_cell(base, k_lo, k_hi, cb + x0) : k_lo;
         for (int x = x0; x < x1; x += 32) {
-          uint32_t* cp = cells + (size_t)x * (GP + 1);
+          uint32_t* cp = cells + (size_t)x * kCW;
 #if MOC_V2_NOCOUNT
           constexpr uint32_t cnt = 0u;
           uint32_t any = 0u;
@@ -964,7 +972,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
           for (int g = 0; g < G; ++g) {
             sum[g] = cp[g];
 #pragma unroll
-            for (int c = 1; c < kTileCopies; ++c) sum[g] += cp[(size_t)c * cap * (GP + 1) + g];
+            for (int c = 1; c < kTileCopies; ++c) sum[g] += cp[(size_t)c * cap * kCW + g];
             any |= sum[g];
           }
           if (!any) continue;
@@ -984,7 +992,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
             raw[g] = g < G ? sum[g] : 0u;  // pad words are never written
             if (g < G)
 #pragma unroll
-              for (int c = 0; c < kTileCopies; ++c) cp[(size_t)c * cap * (GP + 1) + g] = 0u;
+              for (int c = 0; c < kTileCopies; ++c) cp[(size_t)c * cap * kCW + g] = 0u;
 #else
             raw[g] = g < G ? cp[g] : kMagicBits * cnt;  // pad words are never written
             if (g < G) cp[g] = 0u;
