@@ -438,9 +438,13 @@ struct WalkState {
 // the track ends.  UP: the track climbs (cot > 0).
 template <int G, int GP, bool UP>
 __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, GP>& ph, const KSeg* TF, double z0,
-                                               double tn, double isn, int c_hi) {
+                                               double tn, double isn, int c_hi, int skew) {
   while (true) {
     if (w.pc >= c_hi) return;
+    if (skew > 0) {  // lane skew: sit out this trip (see walk_chunk)
+      --skew;
+      continue;
+    }
     if (w.done) {
       if (w.pc >= 0) {
         w.emit_to(ph, w.pL);
@@ -519,9 +523,13 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
 // merged list is the reverse of the forward one (reading Q22b).
 template <int G, int GP, bool UP>
 __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, GP>& ph, const KSeg* TF,
-                                               const KSeg* TB, double z0, double tn, double isn, int c_lo) {
+                                               const KSeg* TB, double z0, double tn, double isn, int c_lo, int skew) {
   while (true) {
     if ((unsigned)w.pc < (unsigned)c_lo) return;
+    if (skew > 0) {
+      --skew;
+      continue;
+    }
     if (w.done) {
       if (w.pc >= 0) {
         w.emit_to(ph, w.pL + w.carry);
@@ -651,12 +659,20 @@ __device__ __forceinline__ void replay_chunk(Replay<GP>& r, Physics<G, GP>& ph, 
   }
 }
 
-// one direction of one track through one chunk
+// one direction of one track through one chunk.  Lane skew (MOC_V2_LANE_SKEW = m > 1):
+// lane L starts the chunk L mod m loop trips late.  A warp's lanes advance one raw piece
+// per trip in lockstep, and neighbouring lanes (members 2^lg apart) otherwise sit in the
+// same tally cell at the same trip; offset by a piece they are in different cells, so the
+// tile atomics of one warp instruction conflict less (m - 1 extra trips per chunk).
+#ifndef MOC_V2_LANE_SKEW
+#define MOC_V2_LANE_SKEW 1
+#endif
 template <int G, int GP, bool UP>
 __device__ __forceinline__ void walk_chunk(int dir, WalkState<G, GP>& w, Physics<G, GP>& ph, const KSeg* TF,
                                            const KSeg* TB, double z0, double tn, double isn, int c_lo, int c_hi) {
-  if (dir == 0) walk_fwd_chunk<G, GP, UP>(w, ph, TF, z0, tn, isn, c_hi);
-  else walk_bwd_chunk<G, GP, UP>(w, ph, TF, TB, z0, tn, isn, c_lo);
+  const int skew = MOC_V2_LANE_SKEW > 1 ? (int)(threadIdx.x & 31) % MOC_V2_LANE_SKEW : 0;
+  if (dir == 0) walk_fwd_chunk<G, GP, UP>(w, ph, TF, z0, tn, isn, c_hi, skew);
+  else walk_bwd_chunk<G, GP, UP>(w, ph, TF, TB, z0, tn, isn, c_lo, skew);
 }
 
 // largest k in [k_lo, k_hi) with base[k] <= c (the 2D segment owning tile cell c)
