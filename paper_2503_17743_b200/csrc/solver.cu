@@ -501,6 +501,7 @@ struct moc_solver {
   uint32_t* d_cost = nullptr;
   uint8_t* d_mat = nullptr;
   float *d_qt = nullptr, *d_phi = nullptr, *d_fold = nullptr, *d_fnew = nullptr;
+  cudaTextureObject_t qtex = 0;  // d_qt as float4 texture (GP = 8; the MOC_V2_QTEX gather)
   double* d_phi64 = nullptr;  // [J][G] staging for moc_get_scalar_flux (allocated on first use)
   double *d_tally = nullptr, *d_vol = nullptr;
   float* d_psi[2] = {nullptr, nullptr};
@@ -610,6 +611,7 @@ void run_sweep(moc_solver* s) {
     a.link = s->d_link;
     a.mat = s->d_mat;
     a.qt = s->d_qt;
+    a.qtex = s->qtex;
     a.qmax_t = s->d_qmax_t;
     a.psi_in = s->d_psi[in];
     a.psi_out = s->d_psi[out];
@@ -806,6 +808,7 @@ void destroy(moc_solver* s) {
                   s->d_vol, s->d_psi[0], s->d_psi[1], s->d_sc, s->d_part_a, s->d_part_b, s->d_part_c, s->d_hist,
                   s->d_units, s->d_counter, s->d_rmax, s->d_qmax_t, s->d_tally32, s->d_err,
                   s->d_unit_maxq, s->d_unit_exp, s->d_store, s->d_phi64};
+  if (s->qtex) cudaDestroyTextureObject(s->qtex);
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : s->ev)
@@ -959,6 +962,16 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     upload(m8.data(), s->d_mat, s->J, st);
     const size_t JG = (size_t)s->J * s->GP;
     s->d_qt = dmalloc<float>(JG, B);
+    if (s->GP == 8 && JG / 4 < (int64_t(1) << 27)) {
+      cudaResourceDesc rd{};
+      rd.resType = cudaResourceTypeLinear;
+      rd.res.linear.devPtr = s->d_qt;
+      rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+      rd.res.linear.sizeInBytes = sizeof(float) * (size_t)JG;
+      cudaTextureDesc td{};
+      td.readMode = cudaReadModeElementType;
+      CUDA_OK(cudaCreateTextureObject(&s->qtex, &rd, &td, nullptr));
+    }
     s->d_phi = dmalloc<float>(JG, B);
     s->d_tally = dmalloc<double>(JG, B);
     s->d_vol = dmalloc<double>(s->J, B);

@@ -54,6 +54,9 @@ constexpr uint64_t kNoExp = ~0ull;
 #ifndef MOC_V2_NOCOUNT
 #define MOC_V2_NOCOUNT 1
 #endif
+#ifndef MOC_V2_QTEX
+#define MOC_V2_QTEX 1
+#endif
 #ifndef MOC_V2_SIG_CONST
 #define MOC_V2_SIG_CONST 1
 #endif
@@ -145,6 +148,7 @@ struct V2Args {
   const uint32_t* link;
   const uint8_t* mat;
   const float* qt;      // [J][GP]; for G < GP slot G carries the FSR's material index bits
+  cudaTextureObject_t qtex;  // qt as a float4 texture (MOC_V2_QTEX: the gather on the TEX pipe)
   const float* qmax_t;  // [T2][GP] max qtilde over the FSRs under 2D track t
   const float* psi_in;
   float* psi_out;
@@ -262,6 +266,7 @@ struct Physics {
   float2 scl2[NP];
   const uint8_t* mat;
   const float* qt;
+  cudaTextureObject_t qtex;
   int cb;        // first cell of the current chunk (tile cell 0)
   int tile_off;  // byte offset of the tile in the dynamic buffer
   uint32_t tsa;  // shared address of the tile minus cb cells (cell pc at tsa + pc * 4 cell_words)
@@ -418,11 +423,24 @@ struct WalkState {
   }
   // make raw piece (k, l) the pending segment: its cell, source and material (staged:
   // only the cell; Eq. 3 reads the chunk's stage)
-  __device__ __forceinline__ void set_pending(int jx, int cy, int ll, const uint8_t* mat, const float* qt) {
+  __device__ __forceinline__ void set_pending(int jx, int cy, int ll, const uint8_t* mat, const float* qt,
+                                              cudaTextureObject_t qtex) {
     pc = cy + ll;
     if constexpr (!staged(G, GP)) {
       const int64_t j = (int64_t)(jx + ll);
+#if MOC_V2_QTEX
+      if constexpr (GP == 8) {
+        // the source gather through the texture pipe (its own L1TEX data path; the LSU
+        // data pipe carries the tally atomics)
+        const float4 a = tex1Dfetch<float4>(qtex, (int)(2 * j)), b = tex1Dfetch<float4>(qtex, (int)(2 * j + 1));
+        pq[0] = a.x; pq[1] = a.y; pq[2] = a.z; pq[3] = a.w;
+        pq[4] = b.x; pq[5] = b.y; pq[6] = b.z; pq[7] = b.w;
+      } else {
+        load_q<GP>(qt, j, pq);
+      }
+#else
       load_q<GP>(qt, j, pq);
+#endif
       if constexpr (G < GP) pm = __float_as_int(pq[G]);  // material index rides in the pad slot
       else pm = mat[j];
     }
@@ -453,7 +471,7 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
       } else if (w.fkl >= 0) {  // all-sliver track: one segment at its first piece
         const KSeg e = TF[w.fkl & 0xffff];
         if (e.ky + (w.fkl >> 16) >= c_hi) return;
-        w.set_pending(e.kx, e.ky, w.fkl >> 16, ph.mat, ph.qt);
+        w.set_pending(e.kx, e.ky, w.fkl >> 16, ph.mat, ph.qt, ph.qtex);
         w.emit_to(ph, w.carry);
         w.pc = -1;
         w.fkl = -1;
@@ -484,7 +502,7 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
       if (w.pc >= 0) w.emit_to(ph, w.pL);
       w.pL = L3 + w.carry;
       w.carry = 0.f;
-      w.set_pending(w.kx, w.ky, w.l, ph.mat, ph.qt);
+      w.set_pending(w.kx, w.ky, w.l, ph.mat, ph.qt, ph.qtex);
     }
     if (last) {
       w.done = 1;
@@ -538,7 +556,7 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, G
       } else if (w.fkl >= 0) {  // all-sliver track: emitted in the chunk of its first piece
         const KSeg e = TF[w.fkl & 0xffff];
         if (e.ky + (w.fkl >> 16) < c_lo) return;
-        w.set_pending(e.kx, e.ky, w.fkl >> 16, ph.mat, ph.qt);
+        w.set_pending(e.kx, e.ky, w.fkl >> 16, ph.mat, ph.qt, ph.qtex);
         w.emit_to(ph, w.carry);
         w.pc = -1;
         w.fkl = -1;
@@ -562,7 +580,7 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, G
       if (w.pc >= 0) w.emit_to(ph, w.pL);
       w.pL = L3 + w.carry;
       w.carry = 0.f;
-      w.set_pending(w.kx, w.ky, w.l, ph.mat, ph.qt);
+      w.set_pending(w.kx, w.ky, w.l, ph.mat, ph.qt, ph.qtex);
     }
     if (last) {
       w.done = 1;
@@ -868,6 +886,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     for (int g = 0; g < 2 * Physics<G, GP>::NP; ++g) ph.scl(g) = g < G ? sh_scale[g] : 0.f;
     ph.mat = a.mat;
     ph.qt = a.qt;
+    ph.qtex = a.qtex;
     ph.tile_off = a.tile_off;
     const uint32_t tile_sa = (uint32_t)__cvta_generic_to_shared(dsm) + (uint32_t)a.tile_off;
     const uint32_t stage_sa = (uint32_t)__cvta_generic_to_shared(dsm) + (uint32_t)a.stage_off;
