@@ -54,6 +54,9 @@ constexpr uint64_t kNoExp = ~0ull;
 #ifndef MOC_V2_NOCOUNT
 #define MOC_V2_NOCOUNT 1
 #endif
+#ifndef MOC_V2_KTEX
+#define MOC_V2_KTEX 0
+#endif
 #ifndef MOC_V2_QTEX
 #define MOC_V2_QTEX 1
 #endif
@@ -149,6 +152,7 @@ struct V2Args {
   const uint8_t* mat;
   const float* qt;      // [J][GP]; for G < GP slot G carries the FSR's material index bits
   cudaTextureObject_t qtex;  // qt as a float4 texture (MOC_V2_QTEX: the gather on the TEX pipe)
+  cudaTextureObject_t ktf, ktb;  // per global 2D segment {s_end | s_start, region * NL} (MOC_V2_KTEX)
   const float* qmax_t;  // [T2][GP] max qtilde over the FSRs under 2D track t
   const float* psi_in;
   float* psi_out;
@@ -267,6 +271,8 @@ struct Physics {
   const uint8_t* mat;
   const float* qt;
   cudaTextureObject_t qtex;
+  cudaTextureObject_t ktf, ktb;
+  int sb;        // global index of the unit's first 2D segment (MOC_V2_KTEX fetches)
   int cb;        // first cell of the current chunk (tile cell 0)
   int tile_off;  // byte offset of the tile in the dynamic buffer
   uint32_t tsa;  // shared address of the tile minus cb cells (cell pc at tsa + pc * 4 cell_words)
@@ -421,6 +427,19 @@ struct WalkState {
     kx = v.z;
     ky = v.w;
   }
+  // radial step to 2D segment k in the hot loop: MOC_V2_KTEX fetches {s, region * NL}
+  // through the texture pipe and only the per-unit cell offset from shared memory (4 bytes
+  // per lane on the LSU data pipe instead of 16)
+  __device__ __forceinline__ void step(const KSeg* T, cudaTextureObject_t kt, int sb_, int kk) {
+#if MOC_V2_KTEX
+    const int4 v = tex1Dfetch<int4>(kt, sb_ + kk);
+    s_rad = __hiloint2double(v.y, v.x);
+    kx = v.z;
+    ky = T[kk].ky;
+#else
+    load(T[kk]);
+#endif
+  }
   // make raw piece (k, l) the pending segment: its cell, source and material (staged:
   // only the cell; Eq. 3 reads the chunk's stage)
   __device__ __forceinline__ void set_pending(int jx, int cy, int ll, const uint8_t* mat, const float* qt,
@@ -521,7 +540,7 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
 #elif !defined(MOC_V2_BRANCHLESS)
       if (rad) {
         ++w.k;
-        w.load(TF[w.k]);
+        w.step(TF, ph.ktf, ph.sb, w.k);
       } else {
         w.l += UP ? 1 : -1;
         w.s_ax = (ph.plane(w.l + (UP ? 1 : 0)) - z0) * tn;
@@ -599,7 +618,7 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, G
 #elif !defined(MOC_V2_BRANCHLESS)
       if (rad) {
         --w.k;
-        w.load(TB[w.k]);
+        w.step(TB, ph.ktb, ph.sb, w.k);
       } else {
         w.l -= UP ? 1 : -1;
         w.s_ax = (ph.plane(w.l + (UP ? 0 : 1)) - z0) * tn;
@@ -887,6 +906,9 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     ph.mat = a.mat;
     ph.qt = a.qt;
     ph.qtex = a.qtex;
+    ph.ktf = a.ktf;
+    ph.ktb = a.ktb;
+    ph.sb = (int)sb;
     ph.tile_off = a.tile_off;
     const uint32_t tile_sa = (uint32_t)__cvta_generic_to_shared(dsm) + (uint32_t)a.tile_off;
     const uint32_t stage_sa = (uint32_t)__cvta_generic_to_shared(dsm) + (uint32_t)a.stage_off;
