@@ -1001,7 +1001,8 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     upload(m8.data(), s->d_mat, s->J, st);
     const size_t JG = (size_t)s->J * s->GP;
     s->d_qt = dmalloc<float>(JG, B);
-    if (s->GP == 8 && JG / 4 < (int64_t(1) << 27)) {
+    if (s->GP == 8) {
+      if (JG / 4 >= ((size_t)1 << 27)) throw Error(MOC_E_CAPACITY, "more than 2^26 FSRs at 5-8 groups (source texture)");
       cudaResourceDesc rd{};
       rd.resType = cudaResourceTypeLinear;
       rd.res.linear.devPtr = s->d_qt;

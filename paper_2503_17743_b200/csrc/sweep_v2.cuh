@@ -450,7 +450,8 @@ struct WalkState {
 #if MOC_V2_QTEX
       if constexpr (GP == 8) {
         // the source gather through the texture pipe (its own L1TEX data path; the LSU
-        // data pipe carries the tally atomics)
+        // data pipe carries the tally atomics; the solver refuses problems whose sources
+        // exceed a 1D texture, > 2^26 FSRs at GP = 8)
         const float4 a = tex1Dfetch<float4>(qtex, (int)(2 * j)), b = tex1Dfetch<float4>(qtex, (int)(2 * j + 1));
         pq[0] = a.x; pq[1] = a.y; pq[2] = a.z; pq[3] = a.w;
         pq[4] = b.x; pq[5] = b.y; pq[6] = b.z; pq[7] = b.w;
