@@ -175,7 +175,12 @@ typedef struct {
 /* Upload the laydown to `device`, allocate HBM state (boundary psi double buffer,
  * FSR arrays), compute track-based FSR volumes and exact per-track segment counts on
  * the device.  comm == NULL means one GPU; with world > 1 this rank sweeps its
- * contiguous cost-balanced share of the stacks. */
+ * contiguous cost-balanced share of the stacks.
+ * MOC_E_CAPACITY: device memory exhausted, more than 255 axial layers, an axial mesh too
+ * fine for the shared-memory tally tile, or (5-8 groups) more than 2^26 FSRs, the limit
+ * of the 1D texture the sweep gathers FSR sources through.  The small per-problem tables
+ * (cross sections, axial planes) live in the device's constant bank and are re-uploaded
+ * by whichever solver runs next on the device (one solver active per device at a time). */
 int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_stream,
                       const moc_comm_desc* comm, const moc_solver_opts* opts);
 int moc_solver_destroy(moc_solver* s);
