@@ -273,6 +273,18 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = oracle_sample(prob, target_s=args.ref_seconds)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
+    # the unit that binds in practice (from the committed ncu --set full capture of this
+    # kernel and config): the L1 LSU data pipe and the issue rate, next to R_ALU
+    binding = None
+    np_ = os.path.join(ROOT, "profiles", f"ncu_sweep_cfg{args.config}_r1i.json")
+    if os.path.exists(np_):
+        try:
+            mt = json.load(open(np_))[0]["metrics"]
+            binding = {"lsu_data_pipe_busy": float(mt["l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"][0]) / 100,
+                       "issue_active": float(mt["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]) / 100,
+                       "source": os.path.relpath(np_, ROOT)}
+        except Exception:
+            binding = None
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}.json")
     if os.path.exists(tp):
@@ -295,7 +307,8 @@ def run_ours(args):
                      "traffic": traffic, "kernel": "k_sweep", "peak_basis":
                          f"R_ALU = 148 SM x {mhz_max:.0f} MHz ({kind} sm_max) x 128 / (5 + 5/G), SURVEY 8(d)",
                      "frac_at_measured_clock": (achieved / r_alu(G, clocks["sm_mhz"]))
-                     if clocks.get("sm_mhz") else None},
+                     if clocks.get("sm_mhz") else None,
+                     "measured_binding": binding},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "moc_solver_update_materials + moc_iterate(1) + moc_get_scalar_flux"},
         "gpu_launches": tm["launches_per_iter"] * args.steps,
