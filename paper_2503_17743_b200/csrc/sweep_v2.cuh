@@ -54,6 +54,9 @@ constexpr uint64_t kNoExp = ~0ull;
 #ifndef MOC_V2_NOCOUNT
 #define MOC_V2_NOCOUNT 1
 #endif
+#ifndef MOC_V2_F2I
+#define MOC_V2_F2I 0
+#endif
 #ifndef MOC_V2_KTEX
 #define MOC_V2_KTEX 0
 #endif
@@ -381,7 +384,12 @@ struct Physics {
       const float dd = fmaf(-q[g], scl(g), psi(g));
       const float dl = fmaf(-dd, E, dd);  // (psi' - q')(1 - E)
       psi(g) -= dl;
+#if MOC_V2_F2I && MOC_V2_NOCOUNT
+      // fixed-point code by one F2I (XU pipe) instead of FADD + IADD (A/B)
+      asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(ca + 4u * g), "r"((uint32_t)__float2int_rn(dl)));
+#else
       MOC_TILE_ADD(g, __float_as_uint(dl + kMagic));
+#endif
     }
 #else
     const float2 nL = make_float2(-Lf, -Lf);
