@@ -128,7 +128,7 @@ __host__ __device__ constexpr int cell_words(int G, int GP) {
 }
 __host__ __device__ constexpr int tile_cell_bytes(int G, int GP) { return 4 * cell_words(G, GP) * kTileCopies; }
 __host__ __device__ constexpr int cell_bytes(int G, int GP) { return tile_cell_bytes(G, GP) + (staged(G, GP) ? 4 * GP : 0); }
-__host__ __device__ constexpr int cap_max_cells(int G, int GP) { return (56000 / cell_bytes(G, GP)) & ~7; }
+__host__ __device__ constexpr int cap_max_cells(int G, int GP) { return ((224000 / kV2MinBlocks) / cell_bytes(G, GP)) & ~7; }
 
 // members i0, i0 + step, ..., i0 + (n - 1) step of one z-stack (step > 1 interleaves
 // sibling units over one range, spreading a warp's lanes further apart in z)
