@@ -157,9 +157,12 @@ typedef struct {
 } moc_comm_desc;
 
 typedef struct {
-  int32_t schedule;     /* 0 = persistent cost-sorted stack-band units (default),
+  int32_t schedule;     /* 0 = persistent cost-sorted stack-band units, one thread per 3D track,
                            1 = Alg. 2 grid-stride over 3D tracks in Alg. 1 order (paper baseline),
-                           2 = Alg. 2 over tracks sorted by segment count with the §4.3 serpentine */
+                           2 = Alg. 2 over tracks sorted by segment count with the §4.3 serpentine,
+                           3 = stack-collective sweep (one warp per band of a z-stack, lanes own
+                               (2D segment, layer) cells, exponentials shared per cell:
+                               P:68, Eqs. 6-11) */
   int32_t threads, blocks;  /* Alg. 2 launch shape (P:146 default 512 x 512); 0 = default */
   int32_t deterministic;    /* reserved (0) */
   int32_t tile_cells;       /* schedule 0: cap on FSR cells per shared-memory tally chunk
@@ -170,6 +173,9 @@ typedef struct {
                                budget, the rest is traced on the fly */
   int32_t exp_budget_mb;    /* EXP budget in MiB (0 = free device memory after allocation) */
   double exp_fraction;      /* fraction of the budget (0 = the paper's 0.8) */
+  int32_t sc_lanes_per_cell; /* schedule 3: lanes per (2D segment, layer) cell, 1/2/4/8 (0 = per stack) */
+  int32_t sc_psi_cap;        /* schedule 3: boundary-psi band capacity per warp in members (0 = fill
+                                the shared memory of kScMinBlocks CTAs per SM) */
 } moc_solver_opts;
 
 /* Upload the laydown to `device`, allocate HBM state (boundary psi double buffer,
@@ -214,6 +220,14 @@ int moc_get_balance(moc_solver* s, double* production, double* absorption, doubl
  * sequence (uint32 little-endian bytes), plus the sum of lengths (parity vs oracle). */
 int moc_device_trace_checksums(moc_solver* s, int64_t first, int64_t n, int32_t* nseg,
                                uint64_t* hash, double* suml);
+
+/* One sweep of the schedule-3 (stack-collective) kernel in checksum mode: for every slot
+ * (2*track + dir) the number of 3D segments the kernel applied Eq. 3 to and the FNV-1a-64
+ * hash of their FSR ids in travel order (dir 1 = the reverse of dir 0).  nseg/hash are
+ * [2*n_tracks3d] host arrays.  The sweep reads the current state and writes only scratch
+ * state (the next psi buffer and the tally, both rewritten by the next iteration); k,
+ * phi and the current psi are unchanged.  MOC_E_STATE unless schedule == 3. */
+int moc_sweep_checksums(moc_solver* s, int32_t* nseg, uint64_t* hash);
 
 /* Device probe of the sweep's Eq. 3 arithmetic: for host fp32 arrays of length n
  * returns dpsi = (psi - q)(1 - e^{-sigma_t len}) and psi_out = psi - dpsi exactly as the sweep

@@ -77,7 +77,7 @@ def lib():
         L.or_get_counts.argtypes = [vp, P(_Counts)]
         L.or_trace3d.restype = i64
         L.or_trace3d.argtypes = [vp, i64, vp, vp, i64]
-        L.or_track_checksums.argtypes = [vp, i64, i64, vp, vp, vp, vp]
+        L.or_track_checksums.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp]
         L.or_total_segments3d.restype = i64
         L.or_total_segments3d.argtypes = [vp]
         L.or_links3d.restype = C.c_int
@@ -253,8 +253,9 @@ class Oracle:
         if n is None:
             n = self.counts["n_tracks3d"] - first
         nseg, h, sl, ch = np.zeros(n, np.int32), np.zeros(n, np.uint64), np.zeros(n), np.zeros(n)
-        lib().or_track_checksums(self._h, int(first), int(n), _ptr(nseg), _ptr(h), _ptr(sl), _ptr(ch))
-        return dict(nseg=nseg, hash=h, suml=sl, chord=ch)
+        rh = np.zeros(n, np.uint64)
+        lib().or_track_checksums(self._h, int(first), int(n), _ptr(nseg), _ptr(h), _ptr(sl), _ptr(ch), _ptr(rh))
+        return dict(nseg=nseg, hash=h, suml=sl, chord=ch, rhash=rh)
 
     def total_segments3d(self):
         return int(lib().or_total_segments3d(self._h))

@@ -923,7 +923,7 @@ int64_t or_trace3d(void* h, int64_t track, int64_t* fsr, double* len, int64_t ca
 }
 
 void or_track_checksums(void* h, int64_t first, int64_t n, int32_t* nseg, uint64_t* hash, double* suml,
-                        double* chord) {
+                        double* chord, uint64_t* rhash) {
   Oracle* o = (Oracle*)h;
 #pragma omp parallel
   {
@@ -936,6 +936,10 @@ void or_track_checksums(void* h, int64_t first, int64_t n, int32_t* nseg, uint64
       o->trace3d(id, f, l, b, mg);
       nseg[q] = (int32_t)f.size();
       hash[q] = fnv1a_u32_seq(f);
+      if (rhash) {  // the same FNV-1a-64 over the ids in reverse order (backward travel)
+        std::vector<int64_t> fr(f.rbegin(), f.rend());
+        rhash[q] = fnv1a_u32_seq(fr);
+      }
       double s = 0;
       for (double x : l) s += x;
       suml[q] = s;

@@ -79,8 +79,8 @@ void or_get_stacks(void* h, double* z0, int64_t* count, int64_t* first);
 /* explicit 3D segmentation of one track; returns #segments (or -needed if cap too small) */
 int64_t or_trace3d(void* h, int64_t track, int64_t* fsr, double* len, int64_t cap);
 /* per-track n_seg, FNV-1a-64 hash of the FSR id sequence (uint32 LE), sum of lengths, chord */
-void or_track_checksums(void* h, int64_t first, int64_t n, int32_t* nseg, uint64_t* hash,
-                        double* suml, double* chord);
+void or_track_checksums(void* h, int64_t first, int64_t n, int32_t* nseg, uint64_t* hash, double* suml,
+                        double* chord, uint64_t* rhash /* reversed-order hash or NULL */);
 int64_t or_total_segments3d(void* h);
 /* 3D links by geometric matching: link[slot] = target slot or -1 (vacuum) */
 int or_links3d(void* h, int64_t* link, char* err, int64_t errlen);

@@ -60,7 +60,8 @@ class moc_comm_desc(C.Structure):
 class moc_solver_opts(C.Structure):
     _fields_ = [("schedule", C.c_int32), ("threads", C.c_int32), ("blocks", C.c_int32),
                 ("deterministic", C.c_int32), ("tile_cells", C.c_int32), ("exp_mode", C.c_int32),
-                ("exp_budget_mb", C.c_int32), ("exp_fraction", C.c_double)]
+                ("exp_budget_mb", C.c_int32), ("exp_fraction", C.c_double),
+                ("sc_lanes_per_cell", C.c_int32), ("sc_psi_cap", C.c_int32)]
 
 
 class moc_solve_opts(C.Structure):
@@ -127,6 +128,7 @@ SIGNATURES = {
     "moc_solver_comm_buffers": (C.c_int, [_vp, _P(moc_comm_buffers)]),
     "moc_solver_halo_counts": (C.c_int, [_vp, _vp, _vp]),
     "moc_attenuation_probe": (C.c_int, [C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "moc_sweep_checksums": (C.c_int, [_vp, _vp, _vp]),
     "moc_iteration_sweep": (C.c_int, [_vp]),
     "moc_iteration_finish": (C.c_int, [_vp]),
 }
@@ -324,7 +326,8 @@ class Solver:
 
     def __init__(self, problem: Problem, device: int = 0, stream=None, schedule: int = 0, threads: int = 0,
                  blocks: int = 0, rank: int = 0, world: int = 1, tile_cells: int = 0, exp_mode: int = 0,
-                 exp_budget_mb: int = 0, exp_fraction: float = 0.0):
+                 exp_budget_mb: int = 0, exp_fraction: float = 0.0, sc_lanes_per_cell: int = 0,
+                 sc_psi_cap: int = 0):
         L = lib()
         self.problem = problem
         self._h = C.c_void_p()
@@ -334,7 +337,8 @@ class Solver:
                 stream = torch.cuda.current_stream(device).cuda_stream
             except Exception:  # torch without CUDA: legacy default stream
                 stream = 0
-        opts = moc_solver_opts(schedule, threads, blocks, 0, tile_cells, exp_mode, exp_budget_mb, exp_fraction)
+        opts = moc_solver_opts(schedule, threads, blocks, 0, tile_cells, exp_mode, exp_budget_mb, exp_fraction,
+                               sc_lanes_per_cell, sc_psi_cap)
         comm = moc_comm_desc(rank, world, 0)
         rc = L.moc_solver_create(C.byref(self._h), problem.handle, device, C.c_void_p(stream), C.byref(comm),
                                  C.byref(opts))
@@ -446,6 +450,14 @@ class Solver:
         nseg, h, sl = np.zeros(n, np.int32), np.zeros(n, np.uint64), np.zeros(n)
         self._call(lib().moc_device_trace_checksums, int(first), int(n), _p(nseg), _p(h), _p(sl))
         return dict(nseg=nseg, hash=h, suml=sl)
+
+    def sweep_checksums(self):
+        """Schedule 3: one checksum-mode sweep; per slot (2*track + dir) the number of
+        segments the kernel applied and the FNV-1a-64 of their FSR ids in travel order."""
+        n = 2 * self.problem.stats()["n_tracks3d"]
+        nseg, h = np.zeros(n, np.int32), np.zeros(n, np.uint64)
+        self._call(lib().moc_sweep_checksums, _p(nseg), _p(h))
+        return nseg, h
 
     def timings(self) -> dict:
         t = moc_timings()

@@ -2,7 +2,9 @@
 
 Host C++ (laydown, ABI) is compiled with -ffp-contract=off and no fast-math
 (App. A.7: host geometry must round the same way run to run); device code with
--lineinfo so ncu's source page maps to csrc/.
+-fmad=false (no FMA contraction: the device fp64 OTF walk then rounds exactly as the
+host walk and the oracle's -ffp-contract=off geometry; the fp32 physics uses explicit
+fmaf, which is unaffected) and -lineinfo so ncu's source page maps to csrc/.
 """
 from __future__ import annotations
 
@@ -34,7 +36,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
     tmp = target + ".tmp"
-    cmd = [nvcc, ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-o", tmp] + [f"-D{d}" for d in defines] + [
+    cmd = [nvcc, ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-shared", "-o", tmp] + [f"-D{d}" for d in defines] + [
            "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off,-fno-fast-math",
            "-Xptxas", "-v" if verbose else "-O3",
            "-lgomp"] + [os.path.join(CSRC, f) for f in SOURCES]

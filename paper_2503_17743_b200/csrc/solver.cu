@@ -459,6 +459,7 @@ __global__ void k_fill_f32(float* p, int64_t n, float v) {
 }  // namespace
 
 #include "sweep_v2.cuh"
+#include "sweep_sc.cuh"
 
 namespace {
 
@@ -535,6 +536,12 @@ struct moc_solver {
   uint64_t* d_unit_exp = nullptr;
   Rec* d_store = nullptr;
   int64_t exp_units = 0, exp_segments = 0, exp_bytes = 0;
+  // stack-collective sweep (schedule 3, sweep_sc.cuh)
+  ScUnit* d_sc_units = nullptr;
+  uint32_t n_sc_units = 0;
+  size_t sc_smem = 0, sc_smem_hash = 0;
+  int sc_pcap = 0, sc_blocks = 0, sc_blocks_hash = 0;
+  double hmin = 0;
   // multi-GPU (world > 1)
   uint32_t *d_send_slots = nullptr, *d_recv_slots = nullptr;
   int64_t n_send = 0, n_recv = 0;
@@ -601,10 +608,36 @@ void upload_materials(moc_solver* s, const double* sigma_t, const double* sigma_
   s->sigs.assign(sigma_s, sigma_s + (size_t)NM * G * G);
 }
 
+template <int G, int GP, bool HASH = false>
+void run_sweep_sc(moc_solver* s, unsigned long long* hash = nullptr, int32_t* nseg = nullptr) {
+  ScArgs a;
+  a.d = s->dd;
+  a.units = s->d_sc_units;
+  a.n_units = s->n_sc_units;
+  a.counter = s->d_counter;
+  a.link = s->d_link;
+  a.mat = s->d_mat;
+  a.qt = s->d_qt;
+  a.qtex = s->qtex;
+  a.psi_in = s->d_psi[s->cur];
+  a.psi_out = s->d_psi[1 - s->cur];
+  a.tally = s->d_tally32;
+  a.sc = s->d_sc;
+  a.pcap = s->sc_pcap;
+  a.hmin = s->hmin;
+  a.err = s->d_err;
+  a.hash = hash;
+  a.nseg = nseg;
+  k_sweep_sc<G, GP, HASH><<<HASH ? s->sc_blocks_hash : s->sc_blocks, kScThreads, HASH ? s->sc_smem_hash : s->sc_smem,
+                            s->stream>>>(a);
+}
+
 template <int G, int GP>
 void run_sweep(moc_solver* s) {
   const int in = s->cur, out = 1 - s->cur;
-  if (s->opts.schedule == 0) {
+  if (s->opts.schedule == 3) {
+    run_sweep_sc<G, GP>(s);
+  } else if (s->opts.schedule == 0) {
     V2Args a;
     a.d = s->dd;
     a.units = s->d_units;
@@ -681,13 +714,15 @@ void v2_configure(moc_solver* s) {
 template <int G, int GP>
 void iter_sweep_half(moc_solver* s, bool time_it) {
   ensure_constants(s);
-  const bool v2 = s->opts.schedule == 0;
+  const bool v2 = s->opts.schedule == 0, f32t = v2 || s->opts.schedule == 3;
   const int nb = s->nb_fsr;
   k_source<G, GP><<<nb, 256, 0, s->stream>>>(s->J, s->d_mat, s->d_phi, s->d_vol, s->d_sc, s->d_qt, s->d_fold,
                                              s->d_part_a);
   if (v2) {
     k_region_qmax<G, GP><<<64, 256, 0, s->stream>>>(s->J / s->NL, s->NL, s->d_qt, s->d_rmax);
     k_track_qmax<G, GP><<<64, 256, 0, s->stream>>>(s->T2, s->d_t_seg, s->d_seg_region, s->d_rmax, s->d_qmax_t);
+  }
+  if (f32t) {
     CUDA_OK(cudaMemsetAsync(s->d_tally32, 0, sizeof(float) * s->J * s->GP, s->stream));
     CUDA_OK(cudaMemsetAsync(s->d_counter, 0, 2 * sizeof(uint32_t), s->stream));
   } else {
@@ -711,7 +746,7 @@ void iter_sweep_half(moc_solver* s, bool time_it) {
 template <int G, int GP>
 void iter_finish_half(moc_solver* s) {
   ensure_constants(s);
-  const bool v2 = s->opts.schedule == 0;
+  const bool v2 = s->opts.schedule == 0 || s->opts.schedule == 3;  // fp32 tally
   const int nb = s->nb_fsr;
   if (s->comm.world > 1) {
     if (s->n_recv) k_halo_move<<<256, 256, 0, s->stream>>>(s->d_psi[1 - s->cur], s->d_recv_slots, s->n_recv, GP,
@@ -776,6 +811,114 @@ iter_fn pick_iter(int G) {
   }
 }
 
+// schedule 3 (sweep_sc.cuh): shared memory per CTA = the warps' psi bands (+ hash state
+// for the checksum variant); kScMinBlocks CTAs per SM
+template <int G, int GP>
+void sc_smem_configure(moc_solver* s) {
+  cudaFuncAttributes fa{};
+  CUDA_OK(cudaFuncGetAttributes(&fa, k_sweep_sc<G, GP, false>));
+  const size_t per_cta = (228 * 1024) / kScMinBlocks - 1024 - fa.sharedSizeBytes;
+  constexpr int NH = ScH<G>::NH;
+  int pcap = s->opts.sc_psi_cap > 0 ? s->opts.sc_psi_cap : (int)(per_cta / ((size_t)kScWarps * NH * 16));
+  pcap = std::max(32, pcap & ~31);
+  s->sc_pcap = pcap;
+  s->sc_smem = (size_t)kScWarps * NH * pcap * 16;
+  s->sc_smem_hash = s->sc_smem + (size_t)kScWarps * pcap * 12;
+  CUDA_OK(cudaFuncSetAttribute(k_sweep_sc<G, GP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->sc_smem));
+  CUDA_OK(cudaFuncSetAttribute(k_sweep_sc<G, GP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)s->sc_smem_hash));
+  int per_sm = 0, per_sm_h = 0, dev = 0, nsm = 0;
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_sc<G, GP, false>, kScThreads, s->sc_smem));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_h, k_sweep_sc<G, GP, true>, kScThreads,
+                                                        s->sc_smem_hash));
+  if (per_sm < 1 || per_sm_h < 1) throw Error(MOC_E_CAPACITY, "stack-collective sweep does not fit on an SM");
+  CUDA_OK(cudaGetDevice(&dev));
+  CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  s->sc_blocks = nsm * per_sm;
+  s->sc_blocks_hash = nsm * per_sm_h;
+}
+
+void sc_smem_configure_any(moc_solver* s) {
+  switch (s->G) {
+    case 1: return sc_smem_configure<1, 1>(s);
+    case 2: return sc_smem_configure<2, 2>(s);
+    case 3: return sc_smem_configure<3, 4>(s);
+    case 4: return sc_smem_configure<4, 4>(s);
+    case 5: return sc_smem_configure<5, 8>(s);
+    case 6: return sc_smem_configure<6, 8>(s);
+    case 7: return sc_smem_configure<7, 8>(s);
+    default: return sc_smem_configure<8, 8>(s);
+  }
+}
+
+// Work units of the stack-collective sweep: bands of B consecutive members of one stack,
+// with R = 2^lgR lanes per cell.  A band's members in one column span
+// (B - 1) dz + rho_max in z (rho_max = widest 2D segment of t x |cot|), so it touches at
+// most floor(((B - 1) dz + rho_max) / h_min) + 2 layers: B is the largest band whose
+// cells fit C = 32 / R lanes' cells and whose psi fits the warp's share of shared memory;
+// R is the smallest (most members per lane and cell) for which such a band fits the
+// psi capacity.  Units are sorted by exact segment count, descending.
+void sc_configure(moc_solver* s, const Geometry& g, const Laydown& L, const std::vector<int32_t>& owner) {
+  int64_t& Bytes = s->dev_bytes;
+  cudaStream_t st = s->stream;
+  sc_smem_configure_any(s);
+  double hmin = 1e300;
+  for (int l = 0; l < g.NL; ++l) hmin = std::min(hmin, g.planes[l + 1] - g.planes[l]);
+  s->hmin = hmin;
+  if (g.NL + 1 > kMaxPlanes) throw Error(MOC_E_CAPACITY, "more than 255 axial layers");
+  std::vector<ScUnit> units;
+  const int forced = s->opts.sc_lanes_per_cell;
+  if (forced != 0 && forced != 1 && forced != 2 && forced != 4 && forced != 8)
+    throw Error(MOC_E_PARAM, "sc_lanes_per_cell must be 0, 1, 2, 4 or 8");
+  for (int64_t q = 0; q < s->S; ++q) {
+    if (!owner.empty() && owner[q] != s->comm.rank) continue;
+    const int64_t cnt = L.st_cnt[q];
+    if (cnt == 0) continue;
+    const int64_t t = q / L.N, n = q % L.N;
+    const int64_t an = (int64_t)L.t_a[t] * L.N + n;
+    double wmax = 0, prev = 0;
+    for (int64_t k = L.t_seg[t]; k < L.t_seg[t + 1]; ++k) {
+      wmax = std::max(wmax, L.seg_send[k] - prev);
+      prev = L.seg_send[k];
+    }
+    const double D = L.an_dz[an], rho = wmax * std::fabs(L.an_cot[an]);
+    int lgR = -1;
+    int64_t Bsel = 0;
+    for (int lg = 0; lg <= 3; ++lg) {
+      if (forced > 0 && (1 << lg) != forced) continue;
+      const int C = 32 >> lg;
+      const double room = (C - 2) * hmin - rho;
+      if (room < 0) continue;
+      const int64_t Bmax = (int64_t)std::floor(room / D) + 1;
+      if (Bmax <= s->sc_pcap || lg == 3 || forced > 0) {
+        lgR = lg;
+        Bsel = std::min<int64_t>(Bmax, s->sc_pcap);
+        break;
+      }
+    }
+    if (lgR < 0 || Bsel < 1)
+      throw Error(MOC_E_CAPACITY, "stack-collective sweep: a 2D segment rises through more layers than a warp has cells");
+    for (int64_t b0 = 0; b0 < cnt; b0 += Bsel)
+      units.push_back(ScUnit{(uint32_t)q, (uint32_t)b0, (uint32_t)std::min<int64_t>(Bsel, cnt - b0), (uint32_t)lgR});
+  }
+  s->n_sc_units = (uint32_t)units.size();
+  s->d_sc_units = dmalloc<ScUnit>(units.size(), Bytes);
+  upload(units.data(), s->d_sc_units, sizeof(ScUnit) * units.size(), st);
+  uint32_t* keys = dmalloc<uint32_t>(units.size(), Bytes);
+  k_sc_unit_cost<<<1024, 256, 0, st>>>(s->d_sc_units, s->n_sc_units, s->d_st_first, s->d_cost, keys);
+  CUDA_OK(cudaGetLastError());
+  auto pol = thrust::cuda::par.on(st);
+  thrust::stable_sort_by_key(pol, thrust::device_ptr<uint32_t>(keys), thrust::device_ptr<uint32_t>(keys) + units.size(),
+                             thrust::device_ptr<ScUnit>(s->d_sc_units), thrust::greater<uint32_t>());
+  CUDA_OK(cudaStreamSynchronize(st));
+  cudaFree(keys);
+  Bytes -= 4 * (int64_t)units.size();
+  s->d_counter = dmalloc<uint32_t>(2, Bytes);
+  s->d_err = dmalloc<int>(1, Bytes);
+  CUDA_OK(cudaMemsetAsync(s->d_err, 0, sizeof(int), st));
+  s->d_tally32 = dmalloc<float>((size_t)s->J * s->GP + 8, Bytes);  // + tail for the leakage
+}
+
 void v2_configure_any(moc_solver* s) {
   switch (s->G) {
     case 1: return v2_configure<1, 1>(s);
@@ -811,7 +954,8 @@ void destroy(moc_solver* s) {
                   s->d_link, s->d_work, s->d_cost, s->d_mat, s->d_qt, s->d_phi, s->d_fold, s->d_fnew, s->d_tally,
                   s->d_vol, s->d_psi[0], s->d_psi[1], s->d_sc, s->d_part_a, s->d_part_b, s->d_part_c, s->d_hist,
                   s->d_units, s->d_counter, s->d_rmax, s->d_qmax_t, s->d_tally32, s->d_err,
-                  s->d_unit_maxq, s->d_unit_exp, s->d_store, s->d_phi64, s->d_kf, s->d_kb};
+                  s->d_unit_maxq, s->d_unit_exp, s->d_store, s->d_phi64, s->d_kf, s->d_kb, s->d_sc_units,
+                  s->d_send_slots, s->d_recv_slots, s->d_halo_send, s->d_halo_recv};
   if (s->qtex) cudaDestroyTextureObject(s->qtex);
   if (s->ktf) cudaDestroyTextureObject(s->ktf);
   if (s->ktb) cudaDestroyTextureObject(s->ktb);
@@ -965,7 +1109,8 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       s->d_link = dmalloc<uint32_t>(2 * s->T3, B);
       upload(l32.data(), s->d_link, 4 * 2 * s->T3, st);
       if (s->comm.world > 1) {
-        if (s->opts.schedule != 0) throw Error(MOC_E_PARAM, "multi-GPU runs use schedule 0");
+        if (s->opts.schedule != 0 && s->opts.schedule != 3)
+          throw Error(MOC_E_PARAM, "multi-GPU runs use schedule 0 or 3");
         if (s->comm.rank < 0 || s->comm.rank >= s->comm.world) throw Error(MOC_E_INVALID_ARG, "bad rank");
         std::vector<double> cost;
         partition_stacks(L, s->comm.world, owner, &cost);
@@ -1060,7 +1205,7 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     // --- work list (schedule)
     auto pol = thrust::cuda::par.on(st);
     int sched = s->opts.schedule;
-    if (sched < 0 || sched > 2) throw Error(MOC_E_INVALID_ARG, "schedule must be 0, 1 or 2");
+    if (sched < 0 || sched > 3) throw Error(MOC_E_INVALID_ARG, "schedule must be 0, 1, 2 or 3");
     if (sched == 0) {
       // persistent stack-band units (sweep_v2.cuh), sorted by exact segment count descending
       int64_t max_nk = 0;
@@ -1154,6 +1299,8 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       s->d_rmax = dmalloc<float>((size_t)g.n_regions * s->GP, B);
       s->d_qmax_t = dmalloc<float>((size_t)s->T2 * s->GP, B);
       s->d_tally32 = dmalloc<float>((size_t)s->J * s->GP + 8, B);  // + tail for the leakage
+    } else if (sched == 3) {
+      sc_configure(s, g, L, owner);
     } else {
       s->d_work = dmalloc<uint32_t>(s->T3, B);
       s->nwork = (uint32_t)s->T3;
@@ -1407,13 +1554,50 @@ int moc_get_timings(moc_solver* s, moc_timings* t) {
 
 int moc_solver_comm_buffers(moc_solver* s, moc_comm_buffers* b) {
   if (!s || !b) return MOC_E_INVALID_ARG;
-  b->tally = s->opts.schedule == 0 ? (void*)s->d_tally32 : (void*)s->d_tally;
+  b->tally = s->opts.schedule == 0 || s->opts.schedule == 3 ? (void*)s->d_tally32 : (void*)s->d_tally;
   // fp32 [J][GP] plus one tail element carrying the leakage through the all-reduce
   b->tally_elems = s->J * s->GP + (s->comm.world > 1 ? 1 : 0);
   b->halo_send = s->d_halo_send;
   b->halo_recv = s->d_halo_recv;
   b->halo_elems = std::max(s->n_send, s->n_recv) * s->GP;
   return MOC_OK;
+}
+
+int moc_sweep_checksums(moc_solver* s, int32_t* nseg, uint64_t* hash) {
+  if (!s || !nseg || !hash) return MOC_E_INVALID_ARG;
+  SOLVER_TRY(s, {
+    CUDA_OK(cudaSetDevice(s->device));
+    if (s->opts.schedule != 3) throw Error(MOC_E_STATE, "sweep checksums need schedule 3");
+    ensure_constants(s);
+    const size_t n = 2 * (size_t)s->T3;
+    int64_t B = 0;
+    int32_t* dn = dmalloc<int32_t>(n, B);
+    unsigned long long* dh = dmalloc<unsigned long long>(n, B);
+    CUDA_OK(cudaMemsetAsync(dn, 0, 4 * n, s->stream));
+    CUDA_OK(cudaMemsetAsync(dh, 0, 8 * n, s->stream));
+    CUDA_OK(cudaMemsetAsync(s->d_tally32, 0, sizeof(float) * s->J * s->GP, s->stream));
+    CUDA_OK(cudaMemsetAsync(s->d_counter, 0, 2 * sizeof(uint32_t), s->stream));
+    double sc[SC_N];
+    read_scalars(s, sc);
+    switch (s->G) {
+      case 1: run_sweep_sc<1, 1, true>(s, dh, dn); break;
+      case 2: run_sweep_sc<2, 2, true>(s, dh, dn); break;
+      case 3: run_sweep_sc<3, 4, true>(s, dh, dn); break;
+      case 4: run_sweep_sc<4, 4, true>(s, dh, dn); break;
+      case 5: run_sweep_sc<5, 8, true>(s, dh, dn); break;
+      case 6: run_sweep_sc<6, 8, true>(s, dh, dn); break;
+      case 7: run_sweep_sc<7, 8, true>(s, dh, dn); break;
+      default: run_sweep_sc<8, 8, true>(s, dh, dn); break;
+    }
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpyAsync(nseg, dn, 4 * n, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_OK(cudaMemcpyAsync(hash, dh, 8 * n, cudaMemcpyDeviceToHost, s->stream));
+    // restore the scalars the sweep accumulates into (leakage, emission counter)
+    CUDA_OK(cudaMemcpyAsync(s->d_sc, sc, sizeof(sc), cudaMemcpyHostToDevice, s->stream));
+    CUDA_OK(cudaStreamSynchronize(s->stream));
+    cudaFree(dn);
+    cudaFree(dh);
+  })
 }
 
 int moc_attenuation_probe(int device, int64_t n, const float* psi, const float* q, const float* sigma_t,
@@ -1453,7 +1637,7 @@ int moc_iteration_sweep(moc_solver* s) {
   if (!s) return MOC_E_INVALID_ARG;
   SOLVER_TRY(s, {
     CUDA_OK(cudaSetDevice(s->device));
-    if (s->opts.schedule != 0) throw Error(MOC_E_STATE, "split iterations need schedule 0");
+    if (s->opts.schedule != 0 && s->opts.schedule != 3) throw Error(MOC_E_STATE, "split iterations need schedule 0 or 3");
     pick_sweep_half(s->G)(s, true);
   })
 }
@@ -1462,7 +1646,7 @@ int moc_iteration_finish(moc_solver* s) {
   if (!s) return MOC_E_INVALID_ARG;
   SOLVER_TRY(s, {
     CUDA_OK(cudaSetDevice(s->device));
-    if (s->opts.schedule != 0) throw Error(MOC_E_STATE, "split iterations need schedule 0");
+    if (s->opts.schedule != 0 && s->opts.schedule != 3) throw Error(MOC_E_STATE, "split iterations need schedule 0 or 3");
     pick_finish_half(s->G)(s, false);
   })
 }

@@ -1,0 +1,495 @@
+// sweep_sc.cuh — stack-collective OTF sweep with exponential reuse (
+// the paper's per-z-stack tracing, Eqs. 6-11, rebuilt for sm_100a).
+//
+// Every member of a z-stack (t, n) is the same line z = z0 + i dz + s cot(theta) shifted
+// by i dz (Eq. 5).  In the (s, z) plane of the stack, the FSRs crossed by its members are
+// the rectangles "cell (k, l)" = [s_k, s_k+1] x [P_l, P_l+1] (2D segment k x axial layer l),
+// and which members cross which cell, and with which 3D length, follows from index
+// arithmetic (Eqs. 6-7, 9-10): a member crossing cell (k, l) from its left face to its
+// right face has L = (s_k+1 - s_k)/sin(theta) (Eq. 8), one from its bottom plane to its top
+// plane L = (P_l+1 - P_l)/|cos(theta)| (Eq. 11, reading Q3) — the same for every such
+// member, so their exponentials are evaluated once per cell; only the "corner" pieces
+// (entering through one kind of face and leaving through the other) have member-dependent
+// lengths, linear in i.
+//
+// Work decomposition (one warp = one work unit = a band of B consecutive members of one
+// stack, one direction after the other):
+//   * the band's boundary psi lives in shared memory (two 16-byte halves per member, SoA);
+//   * the warp walks the 2D segments k (columns) in travel order; in each column lane
+//     (cell c, r) owns cell (k, L_lo + c) — R lanes per cell, C = 32/R cells per warp — and
+//     applies Eq. 3 to that cell's members (those with member index = r mod R) with the
+//     tally of Eq. 4 accumulated in REGISTERS (no shared-memory atomics);
+//   * a member's pieces inside one column are ordered by "sub-phase" q = layer - entry
+//     layer: sub-phase 0 = pieces entered through the column's left face, q >= 1 = pieces
+//     entered through a plane after q-1 earlier pieces in the column; sub-phases are
+//     separated by __syncwarp(), so every member's pieces are applied in travel order;
+//   * at the end of the column each cell's tally (summed over its R lanes) is added to the
+//     FSR tally with two red.global.add.v4.f32.
+// Full classes (left->right, bottom->top) use per-cell E = 2^(-sigma' L) and the
+// aggregated update psi' = psi E + q (1 - E), T += (sum psi - n q)(1 - E): two FP32
+// operations per member and group.  Corner pieces: E per member (FMUL + MUFU.EX2) and the
+// 4-op update of the per-track kernel.
+//
+// Frames.  Each (unit, direction) is mapped to a canonical frame in which the members
+// climb (z' increasing along s') and columns are visited in increasing s': the forward
+// direction of a descending stack mirrors z (z' = Z - z), the backward direction mirrors s
+// (s' = L_t - s) and, for an ascending stack, z.  Member index arithmetic (which member is
+// in which cell) uses one fp64 expression U(x) = ceil((x - base_k)/dz) per boundary, the
+// same on every lane, so each member is in exactly one cell per sub-phase.
+//
+// Segment canonicalisation (App. A.7, readings Q22/Q22b).  Rounding can only misplace a
+// member whose crossing lies within ~1e-13 cm of a cell corner, and then the misplaced
+// piece has (near) zero length.  Raw pieces shorter than eps_L are exactly the ones the
+// walk (otf.h) merges into a neighbour, and they are dropped here: the member's FSR-id
+// sequence equals the walk's merged sequence (a merge keeps the neighbour's id), lengths
+// differ by < eps_L per merge.  The only candidates are the shortest member of each corner
+// range; when its fp32 length is below a guard, the walk's own fp64 expression (forward
+// walk, otf.h) decides.
+#pragma once
+
+namespace {
+
+constexpr int kScWarps = 4;                  // independent warps (units) per CTA
+constexpr int kScThreads = 32 * kScWarps;
+#ifndef MOC_SC_CTAS_PER_SM
+#define MOC_SC_CTAS_PER_SM 4
+#endif
+constexpr int kScMinBlocks = MOC_SC_CTAS_PER_SM;
+constexpr float kScSliverGuard = 4e-5f;      // fp32 corner length below which fp64 decides
+
+struct ScUnit {
+  uint32_t stack, i0, n, lgR;  // members i0 .. i0+n-1 of the stack; R = 1 << lgR lanes per cell
+};
+
+struct ScArgs {
+  DevData d;
+  const ScUnit* units;
+  uint32_t n_units;
+  uint32_t* counter;
+  const uint32_t* link;
+  const uint8_t* mat;
+  const float* qt;           // [J][GP]; for G < GP slot G carries the FSR's material index bits
+  cudaTextureObject_t qtex;  // qt as a float4 texture (GP == 8)
+  const float* psi_in;
+  float* psi_out;
+  float* tally;              // fp32 [J][GP]
+  double* sc;
+  int pcap;                  // psi capacity per warp (members)
+  double hmin;               // thinnest axial layer
+  int* err;
+  unsigned long long* hash;  // HASH: per slot FNV-1a of the emitted FSR ids, in travel order
+  int32_t* nseg;             // HASH: per slot emitted segment count
+};
+
+template <int G>
+struct ScH {
+  static constexpr int NH = (G + 3) / 4;  // 16-byte halves of a member's psi
+};
+
+// forward-walk length of the raw piece (member z0, physical column k, physical layer lp):
+// the exact fp64 expressions of otf.h / the per-track walk (entry = max of the candidate
+// crossings, exit = min), so the sliver decision is the walk's own
+__device__ __forceinline__ double sc_walk_len(const DevData& d, const double* P, int64_t sb, int k, int lp,
+                                              double z0, double tn, double isn, double Lt, bool up) {
+  double s_in, s_out;
+  if (up) {
+    s_in = (0.0 - z0) * tn;
+    s_out = (d.Z - z0) * tn;
+  } else {
+    s_in = (d.Z - z0) * tn;
+    s_out = (0.0 - z0) * tn;
+  }
+  s_in = s_in > 0.0 ? s_in : 0.0;
+  s_out = s_out < Lt ? s_out : Lt;
+  if (s_out < s_in) s_out = s_in;
+  const double sa = k ? d.seg_send[sb + k - 1] : 0.0;
+  const double sbd = d.seg_send[sb + k];
+  const double pe = up ? P[lp] : P[lp + 1];
+  const double px = up ? P[lp + 1] : P[lp];
+  const double se = (pe - z0) * tn, sx = (px - z0) * tn;
+  double lo = sa > se ? sa : se;
+  lo = lo > s_in ? lo : s_in;
+  double hi = sbd < sx ? sbd : sx;
+  hi = hi < s_out ? hi : s_out;
+  return (hi - lo) * isn;
+}
+
+__device__ __forceinline__ uint64_t sc_fnv(uint64_t h, uint32_t u) {
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    h ^= (uint64_t)((u >> (8 * b)) & 0xffu);
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+template <int G, int GP, bool HASH>
+struct ScCell {
+  static constexpr int NH = ScH<G>::NH;
+  float4* psl;  // psi halves [NH][pcap]
+  int pcap;
+  float q[8], sg[8], T[8];
+  uint32_t j;
+  uint64_t* hh;  // HASH state per member
+  int* hc;
+  uint32_t nem;
+
+  __device__ __forceinline__ void load(int m, float* v) const {
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      const float4 x = psl[h * pcap + m];
+      v[4 * h] = x.x;
+      v[4 * h + 1] = x.y;
+      v[4 * h + 2] = x.z;
+      v[4 * h + 3] = x.w;
+    }
+  }
+  __device__ __forceinline__ void store(int m, const float* v) {
+#pragma unroll
+    for (int h = 0; h < NH; ++h) psl[h * pcap + m] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+  }
+  __device__ __forceinline__ void emit_hash(int m) {
+    if constexpr (HASH) {
+      hh[m] = sc_fnv(hh[m], j);
+      hc[m] += 1;
+    }
+  }
+
+  // members m = a1, a1 + R, ... < b (all = r mod R) in a bank-rotated order: the lanes of
+  // a quarter-warp start on distinct 16-byte bank groups (member m -> group m mod 8)
+  template <class F>
+  __device__ __forceinline__ void visit(int a, int b, int r, int lgR, int c, F&& f) {
+    const int R = 1 << lgR;
+    const int a1 = a + ((r - a) & (R - 1));
+    if (a1 >= b) return;
+    const int n = ((b - 1 - a1) >> lgR) + 1;
+    int i0 = ((((c << lgR) + r - a1) & 7) >> lgR);
+    if (i0 >= n) i0 = 0;
+    int idx = i0;
+#pragma unroll 1
+    for (int it = 0; it < n; ++it) {
+      f(a1 + (idx << lgR));
+      idx = idx + 1 == n ? 0 : idx + 1;
+    }
+  }
+
+  // shared-E class: psi' = psi E + q (1 - E); T += (sum psi - n q) F, F = 1 - E
+  template <int dummy = 0>
+  __device__ __forceinline__ void full(int a, int b, int r, int lgR, int c, float L) {
+    if (a >= b) return;
+    float E[8], F[8], qc[8], S[8];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float x = sg[g] * L;  // sigma_t log2(e) L
+      E[g] = ex2_approx(-x);
+      // 1 - 2^-x accurately for small x (the per-cell value: no per-member cost)
+      const float y = x * 0.6931471805599453f;
+      const float Fs = y * fmaf(y, fmaf(y, fmaf(y, -1.f / 24.f, 1.f / 6.f), -0.5f), 1.f);
+      F[g] = x < 0.0625f ? Fs : 1.f - E[g];
+      E[g] = x < 0.0625f ? 1.f - Fs : E[g];
+      qc[g] = q[g] * F[g];
+      S[g] = 0.f;
+    }
+    int n = 0;
+    visit(a, b, r, lgR, c, [&](int m) {
+      float v[4 * NH];
+      load(m, v);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        S[g] += v[g];
+        v[g] = fmaf(v[g], E[g], qc[g]);
+      }
+      store(m, v);
+      emit_hash(m);
+      ++n;
+    });
+    const float fn = (float)n;
+#pragma unroll
+    for (int g = 0; g < G; ++g) T[g] = fmaf(fmaf(-fn, q[g], S[g]), F[g], T[g]);
+    nem += n;
+  }
+
+  // corner class: length d(m) * ti with d = d0 + |m - anchor| dz (anchor = shortest member)
+  __device__ __forceinline__ void corner(int a, int b, int r, int lgR, int c, int anchor, float d0, float dzf,
+                                         float ti) {
+    if (a >= b) return;
+    int n = 0;
+    visit(a, b, r, lgR, c, [&](int m) {
+      const float L = fmaf((float)abs(m - anchor), dzf, d0) * ti;
+      float v[4 * NH];
+      load(m, v);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float E = ex2_approx(-sg[g] * L);
+        const float dd = v[g] - q[g];
+        const float dl = fmaf(-dd, E, dd);
+        v[g] -= dl;
+        T[g] += dl;
+      }
+      store(m, v);
+      emit_hash(m);
+      ++n;
+    });
+    nem += n;
+  }
+};
+
+template <int G, int GP, bool HASH>
+__global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a) {
+  extern __shared__ __align__(16) float4 dsm_sc[];
+  __shared__ double shP[2][kMaxPlanes + 1];  // canonical planes: [0] as given, [1] mirrored z' = Z - z
+  __shared__ __align__(16) float shS[kMaxMat * 8];
+  constexpr int NH = ScH<G>::NH;
+  const DevData& d = a.d;
+  const int NL = d.NL;
+  for (int q = threadIdx.x; q <= NL; q += blockDim.x) {
+    shP[0][q] = d.planes[q];
+    shP[1][q] = d.Z - d.planes[NL - q];
+  }
+  for (int q = threadIdx.x; q < kMaxMat * 8; q += blockDim.x) {
+    const int m = q >> 3, g = q & 7;
+    shS[q] = g < G ? c_sigt2[m * kMaxG + g] : 0.f;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pcap = a.pcap;
+  float4* const psl = dsm_sc + (size_t)warp * NH * pcap;
+  uint64_t* const hh = HASH ? reinterpret_cast<uint64_t*>(dsm_sc + (size_t)kScWarps * NH * pcap) + (size_t)warp * pcap
+                            : nullptr;
+  int* const hc = HASH ? reinterpret_cast<int*>(reinterpret_cast<uint64_t*>(dsm_sc + (size_t)kScWarps * NH * pcap) +
+                                                (size_t)kScWarps * pcap) + (size_t)warp * pcap
+                       : nullptr;
+  const float ps = (float)a.sc[SC_PSI_SCALE];
+  double leak = 0.0;
+  uint64_t nemit = 0;
+
+  while (true) {
+    uint32_t u = 0;
+    if (lane == 0) u = atomicAdd(a.counter, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= a.n_units) break;
+    const ScUnit U = a.units[u];
+    const int s = (int)U.stack;
+    const int t = s / d.N, n = s - t * d.N;
+    const int an = d.t_a[t] * d.N + n;
+    const int64_t sb = d.t_seg[t];
+    const int nk = (int)(d.t_seg[t + 1] - sb);
+    const double dz = d.an_dz[an], cot = d.an_cot[an], tn = d.an_tan[an], isn = d.an_invsin[an];
+    const double Lt = d.t_len[t], z0b = d.st_z0[s];
+    const double c = fabs(cot), invD = 1.0 / dz;
+    const float ti = (float)(isn * fabs(tn));  // 3D length per unit of z: 1/|cos(theta)|
+    const float dzf = (float)dz;
+    const int B = (int)U.n, lgR = (int)U.lgR, R = 1 << lgR, C = 32 >> lgR;
+    const bool up = cot > 0;
+    const uint32_t id0 = d.st_first[s] + U.i0;
+    const float cw = d.an_c[an];
+    const int ci = lane >> lgR, r = lane & (R - 1);
+
+    for (int dir = 0; dir < 2; ++dir) {
+      const bool ms = dir == 1;
+      const bool mz = up == (dir == 1);
+      const double* P = shP[mz ? 1 : 0];
+      // canonical member m <-> physical member i0 + (mz ? B-1-m : m)
+      for (int m = lane; m < B; m += 32) {
+        const uint32_t id = id0 + (uint32_t)(mz ? B - 1 - m : m);
+        float v[8];
+        load_q<GP>(a.psi_in, (int64_t)(2 * id + dir), v);
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+          psl[h * pcap + m] = make_float4(v[4 * h] * ps, 4 * h + 1 < G ? v[4 * h + 1] * ps : 0.f,
+                                          4 * h + 2 < G ? v[4 * h + 2] * ps : 0.f, 4 * h + 3 < G ? v[4 * h + 3] * ps : 0.f);
+        if constexpr (HASH) {
+          hh[m] = kFnvInit;
+          hc[m] = 0;
+        }
+      }
+      // canonical height of member 0 at s' = 0
+      const double zc0 = (mz ? d.Z - z0b - (double)(U.i0 + (uint32_t)B - 1) * dz : z0b + (double)U.i0 * dz) -
+                         (ms ? Lt * c : 0.0);
+      int L_lo = 0;
+      __syncwarp();
+      ScCell<G, GP, HASH> cell;
+      cell.psl = psl;
+      cell.pcap = pcap;
+      cell.hh = hh;
+      cell.hc = hc;
+      cell.nem = 0;
+#pragma unroll 1
+      for (int kk = 0; kk < nk; ++kk) {
+        const int k = ms ? nk - 1 - kk : kk;
+        const double s_a = k ? d.seg_send[sb + k - 1] : 0.0;
+        const double s_b = d.seg_send[sb + k];
+        const double S = kk == 0 ? 0.0 : (ms ? Lt - s_b : s_a);
+        const double w = s_b - s_a;
+        const double base = zc0 + S * c, rho = w * c;
+        if (base >= d.Z) break;  // every member of the band has left through the top
+        const double top = base + (double)(B - 1) * dz + rho;
+        if (top <= 0.0) continue;  // no member has entered yet
+        while (L_lo < NL - 1 && P[L_lo + 1] <= base) ++L_lo;
+        int L_hi = L_lo;
+        while (L_hi < NL - 1 && P[L_hi + 1] < top) ++L_hi;
+        if (L_hi - L_lo + 1 > C) {
+          if (lane == 0) atomicAdd(a.err, 1);
+          L_hi = L_lo + C - 1;
+        }
+        const int l = L_lo + ci;
+        const bool act = l <= L_hi;
+        auto Uf = [&](double x) {
+          const int v = __double2int_ru((x - base) * invD);
+          return min(max(v, 0), B);
+        };
+        const uint32_t region = d.seg_region[sb + k];
+        const float Lf = (float)(w * isn);
+#pragma unroll
+        for (int g = 0; g < 8; ++g) cell.T[g] = 0.f;
+        double Pl = 0, Pu = 0;
+        int uPlR = 0, uPuR = 0, lp = 0;
+        if (act) {
+          lp = mz ? NL - 1 - l : l;
+          cell.j = region * (uint32_t)NL + (uint32_t)lp;
+          float qv[8];
+          int mi;
+          if constexpr (GP == 8) {
+            const float4 x0 = tex1Dfetch<float4>(a.qtex, (int)(2 * cell.j)), x1 = tex1Dfetch<float4>(a.qtex, (int)(2 * cell.j + 1));
+            qv[0] = x0.x; qv[1] = x0.y; qv[2] = x0.z; qv[3] = x0.w;
+            qv[4] = x1.x; qv[5] = x1.y; qv[6] = x1.z; qv[7] = x1.w;
+          } else {
+            load_q<GP>(a.qt, (int64_t)cell.j, qv);
+          }
+          if constexpr (G < GP) mi = __float_as_int(qv[G]);
+          else mi = a.mat[cell.j];
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            cell.q[g] = g < G ? qv[g] : 0.f;
+            cell.sg[g] = shS[mi * 8 + g];
+          }
+          Pl = P[l];
+          Pu = P[l + 1];
+          uPlR = Uf(Pl - rho);
+          uPuR = Uf(Pu - rho);
+          // sub-phase 0: members entering through the left face in layer l
+          const int uPl = Uf(Pl), uPu = Uf(Pu);
+          cell.full(uPl, min(uPu, uPuR), r, lgR, ci, Lf);
+          int a0 = max(uPl, uPuR), b0 = uPu;
+          if (a0 < b0) {
+            // left -> top corners: the shortest is the highest member (anchor b0 - 1)
+            const double dtop = Pu - (base + (double)(b0 - 1) * dz);
+            if ((float)dtop * ti < kScSliverGuard) {
+              const int mphys = mz ? B - 1 - (b0 - 1) : b0 - 1;
+              const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
+              if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) --b0;
+            }
+            cell.corner(a0, b0, r, lgR, ci, b0 - 1, (float)(Pu - (base + (double)(b0 - 1) * dz)), dzf, ti);
+          }
+        }
+        const int Q = 1 + (int)(rho / a.hmin);
+#pragma unroll 1
+        for (int q = 1; q <= Q; ++q) {
+          __syncwarp();
+          const int e = l - q;  // entry layer (-1: through the domain bottom)
+          if (act && e >= -1) {
+            const int lo = max(e >= 0 ? Uf(P[e]) : 0, uPlR);
+            const int hi = Uf(P[e + 1]);
+            // bottom -> right corners: the shortest is the lowest member (anchor lo)
+            int a1 = lo;
+            const int b1 = min(hi, uPuR);
+            if (a1 < b1) {
+              const double dbot = base + (double)a1 * dz + rho - Pl;
+              if ((float)dbot * ti < kScSliverGuard) {
+                const int mphys = mz ? B - 1 - a1 : a1;
+                const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
+                if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) ++a1;
+              }
+              if (a1 < b1)
+                cell.corner(a1, b1, r, lgR, ci, a1, (float)(base + (double)a1 * dz + rho - Pl), dzf, ti);
+            }
+            // bottom -> top (full axial)
+            cell.full(max(lo, uPuR), hi, r, lgR, ci, (float)(Pu - Pl) * ti);
+          }
+        }
+        // the cell's tally: sum over its R lanes, c_{a,n} * T -> FSR tally
+        for (int o = 1; o < R; o <<= 1)
+#pragma unroll
+          for (int g = 0; g < G; ++g) cell.T[g] += __shfl_xor_sync(0xffffffffu, cell.T[g], o);
+        if (act && r == 0) {
+          float v[8];
+          bool any = false;
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            v[g] = g < G ? cell.T[g] * cw : 0.f;
+            any |= v[g] != 0.f;
+          }
+          if (any) {
+            float* dst = a.tally + (size_t)cell.j * GP;
+            if constexpr (GP % 4 == 0) {
+#pragma unroll
+              for (int h = 0; h < GP / 4; ++h) red_add_v4(dst + 4 * h, v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+            } else {
+#pragma unroll
+              for (int g = 0; g < G; ++g) atomicAdd(dst + g, v[g]);
+            }
+          }
+        }
+        __syncwarp();
+      }
+      nemit += cell.nem;
+      // outgoing psi of every member (each left through the top or the far end)
+      for (int m = lane; m < B; m += 32) {
+        const uint32_t id = id0 + (uint32_t)(mz ? B - 1 - m : m);
+        float v[8];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+          const float4 x = psl[h * pcap + m];
+          v[4 * h] = x.x;
+          v[4 * h + 1] = x.y;
+          v[4 * h + 2] = x.z;
+          v[4 * h + 3] = x.w;
+        }
+#pragma unroll
+        for (int g = G; g < 8; ++g) v[g] = 0.f;
+        const uint32_t out = a.link[2 * id + dir];
+        if (out != 0xffffffffu) {
+          float* dst = a.psi_out + (size_t)out * GP;
+          if constexpr (GP == 8) {
+            asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(v[0]), "f"(v[1]),
+                         "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                         : "memory");
+          } else {
+#pragma unroll
+            for (int g = 0; g < G; ++g) dst[g] = v[g];
+          }
+        } else {
+          float e = 0.f;
+#pragma unroll
+          for (int g = 0; g < G; ++g) e += v[g];
+          leak += (double)(cw * e);
+        }
+        if constexpr (HASH) {
+          a.hash[2 * id + dir] = hh[m];
+          a.nseg[2 * id + dir] = hc[m];
+        }
+      }
+      __syncwarp();
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    leak += __shfl_xor_sync(0xffffffffu, leak, o);
+    nemit += __shfl_xor_sync(0xffffffffu, nemit, o);
+  }
+  if (lane == 0 && leak != 0.0) atomicAdd(&a.sc[SC_LEAK], leak);
+  if (lane == 0 && nemit) atomicAdd(&a.sc[SC_NEMIT], (double)nemit);
+}
+
+__global__ void k_sc_unit_cost(const ScUnit* units, uint32_t n_units, const uint32_t* st_first, const uint32_t* cost,
+                               uint32_t* key) {
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n_units; u += gridDim.x * blockDim.x) {
+    const ScUnit U = units[u];
+    const uint32_t f = st_first[U.stack] + U.i0;
+    uint32_t c = 0;
+    for (uint32_t i = 0; i < U.n; ++i) c += cost[f + i];
+    key[u] = c;
+  }
+}
+
+}  // namespace
