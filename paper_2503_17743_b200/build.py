@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libmoc3d.so")
 SOURCES = ["laydown.cpp", "partition.cpp", "capi.cpp", "solver.cu"]
-HEADERS = ["host.h", "otf.h", "sweep_v2.cuh"]
+HEADERS = ["host.h", "otf.h", "sweep_v2.cuh", "sweep_sc.cuh"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 

@@ -26,6 +26,24 @@ using namespace moc;
     return MOC_E_INVALID_ARG;                     \
   }
 
+// S:30-35 material rules (shared by moc_set_materials and moc_solver_update_materials)
+void moc::check_materials(int n_mat, int G, const double* sigma_t, const double* sigma_s, const double* nu_sigma_f,
+                          const double* chi) {
+  for (int i = 0; i < n_mat; ++i) {
+    double cs = 0, fs = 0;
+    for (int g = 0; g < G; ++g) {
+      if (!(sigma_t[(size_t)i * G + g] > 0)) throw Error(MOC_E_PARAM, "sigma_t must be > 0");
+      if (!(nu_sigma_f[(size_t)i * G + g] >= 0) || !(chi[(size_t)i * G + g] >= 0))
+        throw Error(MOC_E_PARAM, "nu_sigma_f and chi must be >= 0");
+      for (int h = 0; h < G; ++h)
+        if (!(sigma_s[((size_t)i * G + g) * G + h] >= 0)) throw Error(MOC_E_PARAM, "sigma_s must be >= 0");
+      cs += chi[(size_t)i * G + g];
+      fs += nu_sigma_f[(size_t)i * G + g];
+    }
+    if (fs > 0 && std::fabs(cs - 1.0) > 1e-9) throw Error(MOC_E_PARAM, "chi of a fissile material must sum to 1");
+  }
+}
+
 extern "C" {
 
 int moc_problem_create(moc_problem** out) {
@@ -56,19 +74,7 @@ int moc_set_materials(moc_problem* p, int32_t n_mat, int32_t G, const double* si
     m.sigma_s.assign(sigma_s, sigma_s + (size_t)n_mat * G * G);
     m.nu_sigma_f.assign(nu_sigma_f, nu_sigma_f + (size_t)n_mat * G);
     m.chi.assign(chi, chi + (size_t)n_mat * G);
-    for (int i = 0; i < n_mat; ++i) {
-      double cs = 0, fs = 0;
-      for (int g = 0; g < G; ++g) {
-        if (!(m.sigma_t[(size_t)i * G + g] > 0)) throw Error(MOC_E_PARAM, "sigma_t must be > 0");
-        if (m.nu_sigma_f[(size_t)i * G + g] < 0 || m.chi[(size_t)i * G + g] < 0)
-          throw Error(MOC_E_PARAM, "nu_sigma_f and chi must be >= 0");
-        for (int h = 0; h < G; ++h)
-          if (m.sigma_s[((size_t)i * G + g) * G + h] < 0) throw Error(MOC_E_PARAM, "sigma_s must be >= 0");
-        cs += m.chi[(size_t)i * G + g];
-        fs += m.nu_sigma_f[(size_t)i * G + g];
-      }
-      if (fs > 0 && std::fabs(cs - 1.0) > 1e-9) throw Error(MOC_E_PARAM, "chi of a fissile material must sum to 1");
-    }
+    check_materials(n_mat, G, sigma_t, sigma_s, nu_sigma_f, chi);
     m.set = true;
   })
 }

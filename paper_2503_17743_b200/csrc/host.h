@@ -26,6 +26,10 @@ struct Materials {
   bool set = false;
 };
 
+// sigma_t > 0, sigma_s / nu_sigma_f / chi >= 0, chi of a fissile material sums to 1
+void check_materials(int n_mat, int G, const double* sigma_t, const double* sigma_s, const double* nu_sigma_f,
+                     const double* chi);
+
 struct Geometry {
   int nx = 0, ny = 0;
   double px = 0, py = 0;

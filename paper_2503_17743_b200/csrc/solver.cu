@@ -624,7 +624,7 @@ void run_sweep_sc(moc_solver* s, unsigned long long* hash = nullptr, int32_t* ns
   a.tally = s->d_tally32;
   a.sc = s->d_sc;
   a.pcap = s->sc_pcap;
-  a.hmin = s->hmin;
+  a.inv_hmin = (1.0 / s->hmin) * (1.0 + 1e-12);
   a.err = s->d_err;
   a.hash = hash;
   a.nseg = nseg;
@@ -1350,7 +1350,10 @@ int moc_solver_destroy(moc_solver* s) {
 
 int moc_reset(moc_solver* s) {
   if (!s) return MOC_E_INVALID_ARG;
-  SOLVER_TRY(s, { reset_state(s); })
+  SOLVER_TRY(s, {
+    CUDA_OK(cudaSetDevice(s->device));
+    reset_state(s);
+  })
 }
 
 static void read_scalars(moc_solver* s, double* sc) {
@@ -1433,8 +1436,10 @@ int moc_solver_update_materials(moc_solver* s, const double* sigma_t, const doub
                                 const double* chi) {
   if (!s || !sigma_t || !sigma_s || !nu_sigma_f || !chi) return MOC_E_INVALID_ARG;
   SOLVER_TRY(s, {
-    for (int64_t q = 0; q < (int64_t)s->n_mat * s->G; ++q)
-      if (!(sigma_t[q] > 0)) throw Error(MOC_E_PARAM, "sigma_t must be > 0");
+    CUDA_OK(cudaSetDevice(s->device));
+    check_materials(s->n_mat, s->G, sigma_t, sigma_s, nu_sigma_f, chi);
+    // the pinned staging buffer may still feed an earlier asynchronous constant upload
+    CUDA_OK(cudaStreamSynchronize(s->stream));
     upload_materials(s, sigma_t, sigma_s, nu_sigma_f, chi);
   })
 }
@@ -1442,6 +1447,7 @@ int moc_solver_update_materials(moc_solver* s, const double* sigma_t, const doub
 int moc_get_scalar_flux(moc_solver* s, double* phi) {
   if (!s || !phi) return MOC_E_INVALID_ARG;
   SOLVER_TRY(s, {
+    CUDA_OK(cudaSetDevice(s->device));
     const size_t n = (size_t)s->J * s->G;
     if (!s->d_phi64) s->d_phi64 = dmalloc<double>(n, s->dev_bytes);
     k_phi_f64<<<s->nb_fsr, 256, 0, s->stream>>>(s->d_phi, s->J, s->G, s->GP, s->d_phi64);
@@ -1454,6 +1460,7 @@ int moc_get_scalar_flux(moc_solver* s, double* phi) {
 int moc_get_fsr_volumes(moc_solver* s, double* vol) {
   if (!s || !vol) return MOC_E_INVALID_ARG;
   SOLVER_TRY(s, {
+    CUDA_OK(cudaSetDevice(s->device));
     CUDA_OK(cudaMemcpyAsync(vol, s->d_vol, 8 * s->J, cudaMemcpyDeviceToHost, s->stream));
     CUDA_OK(cudaStreamSynchronize(s->stream));
   })
@@ -1462,6 +1469,7 @@ int moc_get_fsr_volumes(moc_solver* s, double* vol) {
 int moc_get_history(moc_solver* s, double* k_hist, double* res_hist, int32_t cap, int32_t* n) {
   if (!s || !n) return MOC_E_INVALID_ARG;
   SOLVER_TRY(s, {
+    CUDA_OK(cudaSetDevice(s->device));
     double sc[SC_N];
     read_scalars(s, sc);
     int it = std::min((int)sc[SC_ITER], s->hist_cap);
@@ -1507,6 +1515,7 @@ int moc_device_trace_checksums(moc_solver* s, int64_t first, int64_t n, int32_t*
   if (!s || first < 0 || n < 0 || first + n > s->T3) return MOC_E_INVALID_ARG;
   SOLVER_TRY(s, {
     if (n == 0) return MOC_OK;
+    CUDA_OK(cudaSetDevice(s->device));
     int64_t B = 0;
     int32_t* dn = dmalloc<int32_t>(n, B);
     unsigned long long* dh = dmalloc<unsigned long long>(n, B);
@@ -1526,6 +1535,7 @@ int moc_device_trace_checksums(moc_solver* s, int64_t first, int64_t n, int32_t*
 
 int moc_get_timings(moc_solver* s, moc_timings* t) {
   if (!s || !t) return MOC_E_INVALID_ARG;
+  if (cudaSetDevice(s->device) != cudaSuccess) return MOC_E_CUDA;
   t->n_segs3d = s->nseg3;
   t->n_integrations = 2 * s->nseg3 * s->G;
   float ms = 0;

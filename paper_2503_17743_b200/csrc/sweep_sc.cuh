@@ -75,7 +75,7 @@ struct ScArgs {
   float* tally;              // fp32 [J][GP]
   double* sc;
   int pcap;                  // psi capacity per warp (members)
-  double hmin;               // thinnest axial layer
+  double inv_hmin;           // 1 / thinnest axial layer (rounded up)
   int* err;
   unsigned long long* hash;  // HASH: per slot FNV-1a of the emitted FSR ids, in travel order
   int32_t* nseg;             // HASH: per slot emitted segment count
@@ -155,81 +155,121 @@ struct ScCell {
     }
   }
 
-  // members m = a1, a1 + R, ... < b (all = r mod R) in a bank-rotated order: the lanes of
-  // a quarter-warp start on distinct 16-byte bank groups (member m -> group m mod 8)
-  template <class F>
-  __device__ __forceinline__ void visit(int a, int b, int r, int lgR, int c, F&& f) {
+  // members m = a1, a1 + R, ... < b (all = r mod R) in a bank-rotated order (the lanes of
+  // a quarter-warp start on distinct 16-byte bank groups: member m -> group m mod 8), two
+  // members per trip (independent load -> update -> store chains); returns the count
+  template <class F2, class F1>
+  __device__ __forceinline__ int visit(int a, int b, int r, int lgR, int c, F2&& f2, F1&& f1) {
     const int R = 1 << lgR;
     const int a1 = a + ((r - a) & (R - 1));
-    if (a1 >= b) return;
+    if (a1 >= b) return 0;
     const int n = ((b - 1 - a1) >> lgR) + 1;
-    int i0 = ((((c << lgR) + r - a1) & 7) >> lgR);
-    if (i0 >= n) i0 = 0;
-    int idx = i0;
+    int idx = ((((c << lgR) + r - a1) & 7) >> lgR);
+    if (idx >= n) idx = 0;
+    int left = n;
 #pragma unroll 1
-    for (int it = 0; it < n; ++it) {
-      f(a1 + (idx << lgR));
-      idx = idx + 1 == n ? 0 : idx + 1;
+    while (left >= 2) {
+      int i1 = idx + 1;
+      i1 = i1 == n ? 0 : i1;
+      f2(a1 + (idx << lgR), a1 + (i1 << lgR));
+      idx = i1 + 1;
+      idx = idx == n ? 0 : idx;
+      left -= 2;
     }
+    if (left) f1(a1 + (idx << lgR));
+    return n;
   }
 
-  // shared-E class: psi' = psi E + q (1 - E); T += (sum psi - n q) F, F = 1 - E
-  template <int dummy = 0>
+  // shared-E class (Eq. 8 / Eq. 11 pieces of one cell, all of length L):
+  // psi' = psi E + q (1 - E); T += (sum psi - n q)(1 - E)
   __device__ __forceinline__ void full(int a, int b, int r, int lgR, int c, float L) {
     if (a >= b) return;
     float E[8], F[8], qc[8], S[8];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const float x = sg[g] * L;  // sigma_t log2(e) L
-      E[g] = ex2_approx(-x);
-      // 1 - 2^-x accurately for small x (the per-cell value: no per-member cost)
-      const float y = x * 0.6931471805599453f;
-      const float Fs = y * fmaf(y, fmaf(y, fmaf(y, -1.f / 24.f, 1.f / 6.f), -0.5f), 1.f);
-      F[g] = x < 0.0625f ? Fs : 1.f - E[g];
-      E[g] = x < 0.0625f ? 1.f - Fs : E[g];
+      E[g] = ex2_approx(-sg[g] * L);  // 2^(-sigma_t log2(e) L)
+      F[g] = 1.f - E[g];
       qc[g] = q[g] * F[g];
       S[g] = 0.f;
     }
-    int n = 0;
-    visit(a, b, r, lgR, c, [&](int m) {
-      float v[4 * NH];
-      load(m, v);
+    const int n = visit(
+        a, b, r, lgR, c,
+        [&](int m0, int m1) {
+          float v0[4 * NH], v1[4 * NH];
+          load(m0, v0);
+          load(m1, v1);
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        S[g] += v[g];
-        v[g] = fmaf(v[g], E[g], qc[g]);
-      }
-      store(m, v);
-      emit_hash(m);
-      ++n;
-    });
+          for (int g = 0; g < G; ++g) {
+            S[g] += v0[g];
+            S[g] += v1[g];
+            v0[g] = fmaf(v0[g], E[g], qc[g]);
+            v1[g] = fmaf(v1[g], E[g], qc[g]);
+          }
+          store(m0, v0);
+          store(m1, v1);
+          emit_hash(m0);
+          emit_hash(m1);
+        },
+        [&](int m) {
+          float v[4 * NH];
+          load(m, v);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            S[g] += v[g];
+            v[g] = fmaf(v[g], E[g], qc[g]);
+          }
+          store(m, v);
+          emit_hash(m);
+        });
     const float fn = (float)n;
 #pragma unroll
     for (int g = 0; g < G; ++g) T[g] = fmaf(fmaf(-fn, q[g], S[g]), F[g], T[g]);
     nem += n;
   }
 
-  // corner class: length d(m) * ti with d = d0 + |m - anchor| dz (anchor = shortest member)
+  // corner class: length d(m) * ti with d = d0 + |m - anchor| dz (anchor = shortest member);
+  // per member Eq. 3: dpsi = (psi - q)(1 - E), psi -= dpsi, T += dpsi
   __device__ __forceinline__ void corner(int a, int b, int r, int lgR, int c, int anchor, float d0, float dzf,
                                          float ti) {
     if (a >= b) return;
-    int n = 0;
-    visit(a, b, r, lgR, c, [&](int m) {
-      const float L = fmaf((float)abs(m - anchor), dzf, d0) * ti;
-      float v[4 * NH];
-      load(m, v);
+    const int n = visit(
+        a, b, r, lgR, c,
+        [&](int m0, int m1) {
+          const float L0 = fmaf((float)abs(m0 - anchor), dzf, d0) * ti;
+          const float L1 = fmaf((float)abs(m1 - anchor), dzf, d0) * ti;
+          float v0[4 * NH], v1[4 * NH];
+          load(m0, v0);
+          load(m1, v1);
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float E = ex2_approx(-sg[g] * L);
-        const float dd = v[g] - q[g];
-        const float dl = fmaf(-dd, E, dd);
-        v[g] -= dl;
-        T[g] += dl;
-      }
-      store(m, v);
-      emit_hash(m);
-      ++n;
-    });
+          for (int g = 0; g < G; ++g) {
+            const float E0 = ex2_approx(-sg[g] * L0), E1 = ex2_approx(-sg[g] * L1);
+            const float d0_ = v0[g] - q[g], d1_ = v1[g] - q[g];
+            const float l0 = fmaf(-d0_, E0, d0_), l1 = fmaf(-d1_, E1, d1_);
+            v0[g] -= l0;
+            v1[g] -= l1;
+            T[g] += l0;
+            T[g] += l1;
+          }
+          store(m0, v0);
+          store(m1, v1);
+          emit_hash(m0);
+          emit_hash(m1);
+        },
+        [&](int m) {
+          const float L = fmaf((float)abs(m - anchor), dzf, d0) * ti;
+          float v[4 * NH];
+          load(m, v);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float E = ex2_approx(-sg[g] * L);
+            const float dd = v[g] - q[g];
+            const float dl = fmaf(-dd, E, dd);
+            v[g] -= dl;
+            T[g] += dl;
+          }
+          store(m, v);
+          emit_hash(m);
+        });
     nem += n;
   }
 };
@@ -238,7 +278,7 @@ template <int G, int GP, bool HASH>
 __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a) {
   extern __shared__ __align__(16) float4 dsm_sc[];
   __shared__ double shP[2][kMaxPlanes + 1];  // canonical planes: [0] as given, [1] mirrored z' = Z - z
-  __shared__ __align__(16) float shS[kMaxMat * 8];
+  __shared__ __align__(16) float4 shS4[kMaxMat * 2];  // sigma_t log2(e) per material, 8 groups
   constexpr int NH = ScH<G>::NH;
   const DevData& d = a.d;
   const int NL = d.NL;
@@ -248,7 +288,7 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
   }
   for (int q = threadIdx.x; q < kMaxMat * 8; q += blockDim.x) {
     const int m = q >> 3, g = q & 7;
-    shS[q] = g < G ? c_sigt2[m * kMaxG + g] : 0.f;
+    reinterpret_cast<float*>(shS4)[q] = g < G ? c_sigt2[m * kMaxG + g] : 0.f;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -306,7 +346,9 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
       // canonical height of member 0 at s' = 0
       const double zc0 = (mz ? d.Z - z0b - (double)(U.i0 + (uint32_t)B - 1) * dz : z0b + (double)U.i0 * dz) -
                          (ms ? Lt * c : 0.0);
-      int L_lo = 0;
+      // band layer window [L_lo, L_hi]: both ends only rise along the canonical walk
+      // (base and top = base of the next column + (B - 1) dz are non-decreasing)
+      int L_lo = 0, L_hi = 0;
       __syncwarp();
       ScCell<G, GP, HASH> cell;
       cell.psl = psl;
@@ -326,14 +368,15 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
         const double top = base + (double)(B - 1) * dz + rho;
         if (top <= 0.0) continue;  // no member has entered yet
         while (L_lo < NL - 1 && P[L_lo + 1] <= base) ++L_lo;
-        int L_hi = L_lo;
+        if (L_hi < L_lo) L_hi = L_lo;
         while (L_hi < NL - 1 && P[L_hi + 1] < top) ++L_hi;
-        if (L_hi - L_lo + 1 > C) {
+        int Lh = L_hi;
+        if (Lh - L_lo + 1 > C) {
           if (lane == 0) atomicAdd(a.err, 1);
-          L_hi = L_lo + C - 1;
+          Lh = L_lo + C - 1;
         }
         const int l = L_lo + ci;
-        const bool act = l <= L_hi;
+        const bool act = l <= Lh;
         auto Uf = [&](double x) {
           const int v = __double2int_ru((x - base) * invD);
           return min(max(v, 0), B);
@@ -343,7 +386,7 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
 #pragma unroll
         for (int g = 0; g < 8; ++g) cell.T[g] = 0.f;
         double Pl = 0, Pu = 0;
-        int uPlR = 0, uPuR = 0, lp = 0;
+        int uPlR = 0, uPuR = 0, uprev = 0, lp = 0;
         if (act) {
           lp = mz ? NL - 1 - l : l;
           cell.j = region * (uint32_t)NL + (uint32_t)lp;
@@ -358,17 +401,18 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
           }
           if constexpr (G < GP) mi = __float_as_int(qv[G]);
           else mi = a.mat[cell.j];
+          const float4 s0 = shS4[2 * mi], s1 = shS4[2 * mi + 1];
+          cell.sg[0] = s0.x; cell.sg[1] = s0.y; cell.sg[2] = s0.z; cell.sg[3] = s0.w;
+          cell.sg[4] = s1.x; cell.sg[5] = s1.y; cell.sg[6] = s1.z; cell.sg[7] = s1.w;
 #pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            cell.q[g] = g < G ? qv[g] : 0.f;
-            cell.sg[g] = shS[mi * 8 + g];
-          }
+          for (int g = 0; g < 8; ++g) cell.q[g] = g < G ? qv[g] : 0.f;
           Pl = P[l];
           Pu = P[l + 1];
           uPlR = Uf(Pl - rho);
           uPuR = Uf(Pu - rho);
           // sub-phase 0: members entering through the left face in layer l
           const int uPl = Uf(Pl), uPu = Uf(Pu);
+          uprev = uPl;
           cell.full(uPl, min(uPu, uPuR), r, lgR, ci, Lf);
           int a0 = max(uPl, uPuR), b0 = uPu;
           if (a0 < b0) {
@@ -382,14 +426,18 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
             cell.corner(a0, b0, r, lgR, ci, b0 - 1, (float)(Pu - (base + (double)(b0 - 1) * dz)), dzf, ti);
           }
         }
-        const int Q = 1 + (int)(rho / a.hmin);
+        // sub-phases q >= 1: pieces entered through the plane below layer l after q - 1
+        // earlier pieces of the member in this column (at most 1 + rho / h_min of them)
+        const int Q = 1 + (int)(rho * a.inv_hmin);
 #pragma unroll 1
         for (int q = 1; q <= Q; ++q) {
           __syncwarp();
           const int e = l - q;  // entry layer (-1: through the domain bottom)
           if (act && e >= -1) {
-            const int lo = max(e >= 0 ? Uf(P[e]) : 0, uPlR);
-            const int hi = Uf(P[e + 1]);
+            const int hi = uprev;  // Uf(P[e + 1])
+            const int ue = e >= 0 ? Uf(P[e]) : 0;
+            uprev = ue;
+            const int lo = max(ue, uPlR);
             // bottom -> right corners: the shortest is the lowest member (anchor lo)
             int a1 = lo;
             const int b1 = min(hi, uPuR);
@@ -403,7 +451,7 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
               if (a1 < b1)
                 cell.corner(a1, b1, r, lgR, ci, a1, (float)(base + (double)a1 * dz + rho - Pl), dzf, ti);
             }
-            // bottom -> top (full axial)
+            // bottom -> top (full axial, Eq. 11)
             cell.full(max(lo, uPuR), hi, r, lgR, ci, (float)(Pu - Pl) * ti);
           }
         }

@@ -1154,7 +1154,7 @@ __global__ void k_region_qmax(int64_t n_regions, int NL, const float* qt, float*
     const int64_t r = q / G;
     const int g = (int)(q - r * G);
     float m = 0.f;
-    for (int l = 0; l < NL; ++l) m = fmaxf(m, qt[(r * NL + l) * GP + g]);
+    for (int l = 0; l < NL; ++l) m = fmaxf(m, fabsf(qt[(r * NL + l) * GP + g]));  // |q|: robust bound
     rmax[r * GP + g] = m;
   }
 }

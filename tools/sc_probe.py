@@ -70,9 +70,9 @@ def parity(M, oracle, prob, name, iters, **kw):
     return d
 
 
-def timing(M, prob, name, iters=4, **kw):
+def timing(M, prob, name, iters=4, scheds=(0, 3), **kw):
     res = {}
-    for sched in (0, 3):
+    for sched in scheds:
         s = M.Solver(M.Problem(prob), schedule=sched, **(kw if sched == 3 else {}))
         s.iterate(1)
         ms = []
@@ -85,7 +85,8 @@ def timing(M, prob, name, iters=4, **kw):
         res[f"sched{sched}_emitted"] = t["emitted_last"]
         res["integrations"] = t["n_integrations"]
         del s
-    res["sched3_integ_per_s"] = res["integrations"] / (res["sched3_sweep_ms"] * 1e-3)
+    for sched in scheds:
+        res[f"sched{sched}_integ_per_s"] = res["integrations"] / (res[f"sched{sched}_sweep_ms"] * 1e-3)
     return dict(case=name, kind="timing", opts=kw, **res)
 
 
@@ -93,6 +94,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sc_probe.jsonl"))
     ap.add_argument("--what", default="hash,parity,timing")
+    ap.add_argument("--scheds", default="0,3")
+    ap.add_argument("--cfgs", default="4,5")
     args = ap.parse_args()
     import oracle
     import paper_2503_17743_b200 as M
@@ -114,8 +117,8 @@ def main():
                                                        axial_spacing=3.0), "cfg3_reduced_it3", 3))
             out(f, parity(M, oracle, P.config(3), "cfg3_it3", 3))
         if "timing" in what:
-            out(f, timing(M, P.config(4), "cfg4"))
-            out(f, timing(M, P.config(5), "cfg5"))
+            for c in args.cfgs.split(","):
+                out(f, timing(M, P.config(int(c)), f"cfg{c}", scheds=tuple(int(x) for x in args.scheds.split(","))))
 
 
 if __name__ == "__main__":
