@@ -625,6 +625,7 @@ void run_sweep_sc(moc_solver* s, unsigned long long* hash = nullptr, int32_t* ns
   a.sc = s->d_sc;
   a.pcap = s->sc_pcap;
   a.inv_hmin = (1.0 / s->hmin) * (1.0 + 1e-12);
+  a.h_fast = s->hmin * (1.0 - 1e-9);
   a.err = s->d_err;
   a.hash = hash;
   a.nseg = nseg;
@@ -819,10 +820,11 @@ void sc_smem_configure(moc_solver* s) {
   CUDA_OK(cudaFuncGetAttributes(&fa, k_sweep_sc<G, GP, false>));
   const size_t per_cta = (228 * 1024) / kScMinBlocks - 1024 - fa.sharedSizeBytes;
   constexpr int NH = ScH<G>::NH;
-  int pcap = s->opts.sc_psi_cap > 0 ? s->opts.sc_psi_cap : (int)(per_cta / ((size_t)kScWarps * NH * 16));
+  const size_t stage = (size_t)kScWarps * 32 * 64;  // per-warp cell staging (fast path)
+  int pcap = s->opts.sc_psi_cap > 0 ? s->opts.sc_psi_cap : (int)((per_cta - stage) / ((size_t)kScWarps * NH * 16));
   pcap = std::max(32, pcap & ~31);
   s->sc_pcap = pcap;
-  s->sc_smem = (size_t)kScWarps * NH * pcap * 16;
+  s->sc_smem = (size_t)kScWarps * NH * pcap * 16 + stage;
   s->sc_smem_hash = s->sc_smem + (size_t)kScWarps * pcap * 12;
   CUDA_OK(cudaFuncSetAttribute(k_sweep_sc<G, GP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->sc_smem));
   CUDA_OK(cudaFuncSetAttribute(k_sweep_sc<G, GP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -856,8 +858,8 @@ void sc_smem_configure_any(moc_solver* s) {
 // (B - 1) dz + rho_max in z (rho_max = widest 2D segment of t x |cot|), so it touches at
 // most floor(((B - 1) dz + rho_max) / h_min) + 2 layers: B is the largest band whose
 // cells fit C = 32 / R lanes' cells and whose psi fits the warp's share of shared memory;
-// R is the smallest (most members per lane and cell) for which such a band fits the
-// psi capacity.  Units are sorted by exact segment count, descending.
+// R is the smallest for which a band fits at all (R = 1 unless a 2D segment rises through
+// more than 30 layers).  Units are sorted by exact segment count, descending.
 void sc_configure(moc_solver* s, const Geometry& g, const Laydown& L, const std::vector<int32_t>& owner) {
   int64_t& Bytes = s->dev_bytes;
   cudaStream_t st = s->stream;
@@ -890,7 +892,9 @@ void sc_configure(moc_solver* s, const Geometry& g, const Laydown& L, const std:
       const double room = (C - 2) * hmin - rho;
       if (room < 0) continue;
       const int64_t Bmax = (int64_t)std::floor(room / D) + 1;
-      if (Bmax <= s->sc_pcap || lg == 3 || forced > 0) {
+      // fewest lanes per cell whose band fits: every lane then sweeps all members of its
+      // cell (per-cell setup amortised over the most members)
+      if (Bmax >= 1) {
         lgR = lg;
         Bsel = std::min<int64_t>(Bmax, s->sc_pcap);
         break;
@@ -1609,6 +1613,17 @@ int moc_sweep_checksums(moc_solver* s, int32_t* nseg, uint64_t* hash) {
     cudaFree(dh);
   })
 }
+
+#ifdef MOC_SC_STATS
+int moc_debug_sc_stats(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_sc_stats, sizeof(g_sc_stats)) != cudaSuccess) return MOC_E_CUDA;
+  if (reset) {
+    unsigned long long z[16] = {};
+    if (cudaMemcpyToSymbol(g_sc_stats, z, sizeof(z)) != cudaSuccess) return MOC_E_CUDA;
+  }
+  return MOC_OK;
+}
+#endif
 
 int moc_attenuation_probe(int device, int64_t n, const float* psi, const float* q, const float* sigma_t,
                           const float* len, float* psi_out, float* dpsi) {

@@ -52,10 +52,18 @@ namespace {
 constexpr int kScWarps = 4;                  // independent warps (units) per CTA
 constexpr int kScThreads = 32 * kScWarps;
 #ifndef MOC_SC_CTAS_PER_SM
-#define MOC_SC_CTAS_PER_SM 4
+#define MOC_SC_CTAS_PER_SM 3
 #endif
 constexpr int kScMinBlocks = MOC_SC_CTAS_PER_SM;
 constexpr float kScSliverGuard = 4e-5f;      // fp32 corner length below which fp64 decides
+
+// debug statistics build (-DMOC_SC_STATS): per-sweep counts of the work decomposition
+#ifdef MOC_SC_STATS
+__device__ unsigned long long g_sc_stats[16];
+#define SC_STAT(i, v) atomicAdd(&g_sc_stats[i], (unsigned long long)(v))
+#else
+#define SC_STAT(i, v) ((void)0)
+#endif
 
 struct ScUnit {
   uint32_t stack, i0, n, lgR;  // members i0 .. i0+n-1 of the stack; R = 1 << lgR lanes per cell
@@ -76,6 +84,7 @@ struct ScArgs {
   double* sc;
   int pcap;                  // psi capacity per warp (members)
   double inv_hmin;           // 1 / thinnest axial layer (rounded up)
+  double h_fast;             // columns with rho < h_fast take the one-crossing fast path
   int* err;
   unsigned long long* hash;  // HASH: per slot FNV-1a of the emitted FSR ids, in travel order
   int32_t* nseg;             // HASH: per slot emitted segment count
@@ -158,7 +167,7 @@ struct ScCell {
   // members m = a1, a1 + R, ... < b (all = r mod R) in a bank-rotated order (the lanes of
   // a quarter-warp start on distinct 16-byte bank groups: member m -> group m mod 8), two
   // members per trip (independent load -> update -> store chains); returns the count
-  template <class F2, class F1>
+  template <int STAT_TRIP, int STAT_CALL, class F2, class F1>
   __device__ __forceinline__ int visit(int a, int b, int r, int lgR, int c, F2&& f2, F1&& f1) {
     const int R = 1 << lgR;
     const int a1 = a + ((r - a) & (R - 1));
@@ -177,6 +186,13 @@ struct ScCell {
       left -= 2;
     }
     if (left) f1(a1 + (idx << lgR));
+#ifdef MOC_SC_STATS
+    {
+      const unsigned am = __activemask();
+      const int mx = __reduce_max_sync(am, (unsigned)((n + 1) >> 1));
+      if ((threadIdx.x & 31) == __ffs(am) - 1) SC_STAT(STAT_TRIP, mx), SC_STAT(STAT_CALL, 1);
+    }
+#endif
     return n;
   }
 
@@ -192,7 +208,7 @@ struct ScCell {
       qc[g] = q[g] * F[g];
       S[g] = 0.f;
     }
-    const int n = visit(
+    const int n = visit<6, 8>(
         a, b, r, lgR, c,
         [&](int m0, int m1) {
           float v0[4 * NH], v1[4 * NH];
@@ -225,6 +241,7 @@ struct ScCell {
 #pragma unroll
     for (int g = 0; g < G; ++g) T[g] = fmaf(fmaf(-fn, q[g], S[g]), F[g], T[g]);
     nem += n;
+    SC_STAT(3, n);
   }
 
   // corner class: length d(m) * ti with d = d0 + |m - anchor| dz (anchor = shortest member);
@@ -232,7 +249,7 @@ struct ScCell {
   __device__ __forceinline__ void corner(int a, int b, int r, int lgR, int c, int anchor, float d0, float dzf,
                                          float ti) {
     if (a >= b) return;
-    const int n = visit(
+    const int n = visit<7, 9>(
         a, b, r, lgR, c,
         [&](int m0, int m1) {
           const float L0 = fmaf((float)abs(m0 - anchor), dzf, d0) * ti;
@@ -271,6 +288,80 @@ struct ScCell {
           emit_hash(m);
         });
     nem += n;
+    SC_STAT(4, n);
+  }
+
+  // fast-path corner class (rho < h_min): members entering cell l through its left face
+  // and leaving through its top plane P_u into cell l + 1, whose right face they reach
+  // before the next plane.  Piece 1 (cell l): d1(m) = P_u - z_m = d1a + (b - 1 - m) dz;
+  // piece 2 (cell l + 1, only if l + 1 is inside the domain): d2(m) = z_m + rho - P_u =
+  // d2a + (m - a) dz; 3D length = d * ti.  A sliver piece (the walk merges it, App. A.7)
+  // gets length 0 (E = 1: no change) and is not emitted.  q2/sg2 = cell l + 1's source and
+  // sigma_t log2(e) (from the warp's cell staging); T2 = its tally share.
+  __device__ __forceinline__ void corner2(int a, int b, int r, int lgR, int c, float d1a, float d2a, float dzf,
+                                          float ti, bool nxt, int skip1, int skip2, const float4* st2,
+                                          uint32_t j2, float* T2) {
+    if (a >= b) return;
+    float q2[8], sg2[8];
+    {
+      const float4 x0 = st2[0], x1 = st2[32], y0 = st2[64], y1 = st2[96];  // [4][32 lanes] float4
+      q2[0] = x0.x; q2[1] = x0.y; q2[2] = x0.z; q2[3] = x0.w;
+      q2[4] = x1.x; q2[5] = x1.y; q2[6] = x1.z; q2[7] = x1.w;
+      sg2[0] = y0.x; sg2[1] = y0.y; sg2[2] = y0.z; sg2[3] = y0.w;
+      sg2[4] = y1.x; sg2[5] = y1.y; sg2[6] = y1.z; sg2[7] = y1.w;
+    }
+    const float t2 = nxt ? ti : 0.f;  // no second piece above the domain top
+    auto one = [&](int m, float* v) {
+      const float L1 = m == skip1 ? 0.f : fmaf((float)(b - 1 - m), dzf, d1a) * ti;
+      const float L2 = m == skip2 ? 0.f : fmaf((float)(m - a), dzf, d2a) * t2;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float E1 = ex2_approx(-sg[g] * L1);
+        const float e1 = v[g] - q[g];
+        const float l1 = fmaf(-e1, E1, e1);
+        v[g] -= l1;
+        T[g] += l1;
+        const float E2 = ex2_approx(-sg2[g] * L2);
+        const float e2 = v[g] - q2[g];
+        const float l2 = fmaf(-e2, E2, e2);
+        v[g] -= l2;
+        T2[g] += l2;
+      }
+    };
+    auto emit = [&](int m) {
+      if constexpr (HASH) {
+        if (m != skip1) emit_hash(m);
+        if (nxt && m != skip2) {
+          hh[m] = sc_fnv(hh[m], j2);
+          hc[m] += 1;
+        }
+      }
+    };
+    const int n = visit<7, 9>(
+        a, b, r, lgR, c,
+        [&](int m0, int m1) {
+          float v0[4 * NH], v1[4 * NH];
+          load(m0, v0);
+          load(m1, v1);
+          one(m0, v0);
+          one(m1, v1);
+          store(m0, v0);
+          store(m1, v1);
+          emit(m0);
+          emit(m1);
+        },
+        [&](int m) {
+          float v[4 * NH];
+          load(m, v);
+          one(m, v);
+          store(m, v);
+          emit(m);
+        });
+    // emitted pieces: n first + (n second, if inside the domain), minus this lane's slivers
+    nem += nxt ? 2 * n : n;
+    if (skip1 >= 0 && (skip1 & ((1 << lgR) - 1)) == r) --nem;
+    if (nxt && skip2 >= 0 && (skip2 & ((1 << lgR) - 1)) == r) --nem;
+    SC_STAT(4, 2 * n);
   }
 };
 
@@ -294,11 +385,13 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pcap = a.pcap;
   float4* const psl = dsm_sc + (size_t)warp * NH * pcap;
-  uint64_t* const hh = HASH ? reinterpret_cast<uint64_t*>(dsm_sc + (size_t)kScWarps * NH * pcap) + (size_t)warp * pcap
-                            : nullptr;
-  int* const hc = HASH ? reinterpret_cast<int*>(reinterpret_cast<uint64_t*>(dsm_sc + (size_t)kScWarps * NH * pcap) +
-                                                (size_t)kScWarps * pcap) + (size_t)warp * pcap
-                       : nullptr;
+  // per-warp cell staging (fast path), SoA [4][32 lanes] float4: q[0..7], sigma_t log2(e)[0..7]
+  float4* const stg = dsm_sc + (size_t)kScWarps * NH * pcap + (size_t)warp * 32 * 4;
+  float4* const hbase = dsm_sc + (size_t)kScWarps * NH * pcap + (size_t)kScWarps * 32 * 4;
+  uint64_t* const hh = HASH ? reinterpret_cast<uint64_t*>(hbase) + (size_t)warp * pcap : nullptr;
+  int* const hc =
+      HASH ? reinterpret_cast<int*>(reinterpret_cast<uint64_t*>(hbase) + (size_t)kScWarps * pcap) + (size_t)warp * pcap
+           : nullptr;
   const float ps = (float)a.sc[SC_PSI_SCALE];
   double leak = 0.0;
   uint64_t nemit = 0;
@@ -349,6 +442,7 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
       // band layer window [L_lo, L_hi]: both ends only rise along the canonical walk
       // (base and top = base of the next column + (B - 1) dz are non-decreasing)
       int L_lo = 0, L_hi = 0;
+      if (lane == 0) SC_STAT(0, 1);
       __syncwarp();
       ScCell<G, GP, HASH> cell;
       cell.psl = psl;
@@ -377,6 +471,7 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
         }
         const int l = L_lo + ci;
         const bool act = l <= Lh;
+        if (lane == 0) SC_STAT(1, 1), SC_STAT(2, Lh - L_lo + 1);
         auto Uf = [&](double x) {
           const int v = __double2int_ru((x - base) * invD);
           return min(max(v, 0), B);
@@ -385,8 +480,11 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
         const float Lf = (float)(w * isn);
 #pragma unroll
         for (int g = 0; g < 8; ++g) cell.T[g] = 0.f;
+        float T2[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) T2[g] = 0.f;
         double Pl = 0, Pu = 0;
-        int uPlR = 0, uPuR = 0, uprev = 0, lp = 0;
+        int uPl = 0, uPu = 0, uPlR = 0, uPuR = 0, lp = 0;
         if (act) {
           lp = mz ? NL - 1 - l : l;
           cell.j = region * (uint32_t)NL + (uint32_t)lp;
@@ -410,49 +508,109 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
           Pu = P[l + 1];
           uPlR = Uf(Pl - rho);
           uPuR = Uf(Pu - rho);
-          // sub-phase 0: members entering through the left face in layer l
-          const int uPl = Uf(Pl), uPu = Uf(Pu);
-          uprev = uPl;
-          cell.full(uPl, min(uPu, uPuR), r, lgR, ci, Lf);
-          int a0 = max(uPl, uPuR), b0 = uPu;
-          if (a0 < b0) {
-            // left -> top corners: the shortest is the highest member (anchor b0 - 1)
-            const double dtop = Pu - (base + (double)(b0 - 1) * dz);
-            if ((float)dtop * ti < kScSliverGuard) {
-              const int mphys = mz ? B - 1 - (b0 - 1) : b0 - 1;
-              const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
-              if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) --b0;
-            }
-            cell.corner(a0, b0, r, lgR, ci, b0 - 1, (float)(Pu - (base + (double)(b0 - 1) * dz)), dzf, ti);
-          }
+          uPl = Uf(Pl);
+          uPu = Uf(Pu);
         }
-        // sub-phases q >= 1: pieces entered through the plane below layer l after q - 1
-        // earlier pieces of the member in this column (at most 1 + rho / h_min of them)
-        const int Q = 1 + (int)(rho * a.inv_hmin);
-#pragma unroll 1
-        for (int q = 1; q <= Q; ++q) {
+        const bool fast = rho < a.h_fast;  // every member crosses at most one plane here
+        if (fast) {
+          if (!act) {  // finite staging for lanes without a cell (read only with zero lengths)
+#pragma unroll
+            for (int g = 0; g < 8; ++g) cell.q[g] = cell.sg[g] = 0.f;
+          }
+          stg[lane] = make_float4(cell.q[0], cell.q[1], cell.q[2], cell.q[3]);
+          stg[32 + lane] = make_float4(cell.q[4], cell.q[5], cell.q[6], cell.q[7]);
+          stg[64 + lane] = make_float4(cell.sg[0], cell.sg[1], cell.sg[2], cell.sg[3]);
+          stg[96 + lane] = make_float4(cell.sg[4], cell.sg[5], cell.sg[6], cell.sg[7]);
           __syncwarp();
-          const int e = l - q;  // entry layer (-1: through the domain bottom)
-          if (act && e >= -1) {
-            const int hi = uprev;  // Uf(P[e + 1])
-            const int ue = e >= 0 ? Uf(P[e]) : 0;
-            uprev = ue;
-            const int lo = max(ue, uPlR);
-            // bottom -> right corners: the shortest is the lowest member (anchor lo)
-            int a1 = lo;
-            const int b1 = min(hi, uPuR);
-            if (a1 < b1) {
+          if (act) {
+            // members entering through the left face in layer l: full (Eq. 8) ...
+            cell.full(uPl, min(uPu, uPuR), r, lgR, ci, Lf);
+            // ... and corners, left -> top in l, bottom -> right in l + 1
+            const int a0 = max(uPl, uPuR), b0 = uPu;
+            if (a0 < b0) {
+              const bool nxt = l + 1 < NL;
+              const int lp2 = mz ? lp - 1 : lp + 1;
+              const double d1 = Pu - (base + (double)(b0 - 1) * dz);  // shortest piece 1: member b0 - 1
+              const double d2 = base + (double)a0 * dz + rho - Pu;    // shortest piece 2: member a0
+              int skip1 = -1, skip2 = -1;
+              if ((float)d1 * ti < kScSliverGuard) {
+                const int mphys = mz ? B - 1 - (b0 - 1) : b0 - 1;
+                const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
+                if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) skip1 = b0 - 1;
+              }
+              if (nxt && (float)d2 * ti < kScSliverGuard) {
+                const int mphys = mz ? B - 1 - a0 : a0;
+                const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
+                if (sc_walk_len(d, shP[0], sb, k, lp2, z0, tn, isn, Lt, up) < kEpsL) skip2 = a0;
+              }
+              cell.corner2(a0, b0, r, lgR, ci, (float)d1, (float)d2, dzf, ti, nxt, skip1, skip2, stg + ((lane + R) & 31),
+                           region * (uint32_t)NL + (uint32_t)lp2, T2);
+            }
+            // members entering through the domain bottom (canonical z' = 0) in this column
+            if (l == 0 && uPlR < uPl) {
+              int a1 = uPlR;
               const double dbot = base + (double)a1 * dz + rho - Pl;
               if ((float)dbot * ti < kScSliverGuard) {
                 const int mphys = mz ? B - 1 - a1 : a1;
                 const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
                 if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) ++a1;
               }
-              if (a1 < b1)
-                cell.corner(a1, b1, r, lgR, ci, a1, (float)(base + (double)a1 * dz + rho - Pl), dzf, ti);
+              if (a1 < uPl)
+                cell.corner(a1, uPl, r, lgR, ci, a1, (float)(base + (double)a1 * dz + rho - Pl), dzf, ti);
             }
-            // bottom -> top (full axial, Eq. 11)
-            cell.full(max(lo, uPuR), hi, r, lgR, ci, (float)(Pu - Pl) * ti);
+          }
+          // cell l + 1's shares of the corner pieces -> the lanes of cell l + 1
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float x = __shfl_up_sync(0xffffffffu, T2[g], R);
+            if (ci > 0) cell.T[g] += x;
+          }
+        } else {
+          int uprev = uPl;
+          if (act) {
+            // sub-phase 0: members entering through the left face in layer l
+            cell.full(uPl, min(uPu, uPuR), r, lgR, ci, Lf);
+            int a0 = max(uPl, uPuR), b0 = uPu;
+            if (a0 < b0) {
+              // left -> top corners: the shortest is the highest member (anchor b0 - 1)
+              const double dtop = Pu - (base + (double)(b0 - 1) * dz);
+              if ((float)dtop * ti < kScSliverGuard) {
+                const int mphys = mz ? B - 1 - (b0 - 1) : b0 - 1;
+                const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
+                if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) --b0;
+              }
+              cell.corner(a0, b0, r, lgR, ci, b0 - 1, (float)(Pu - (base + (double)(b0 - 1) * dz)), dzf, ti);
+            }
+          }
+          // sub-phases q >= 1: pieces entered through the plane below layer l after q - 1
+          // earlier pieces of the member in this column (at most 1 + rho / h_min of them)
+          const int Q = 1 + (int)(rho * a.inv_hmin);
+#pragma unroll 1
+          for (int q = 1; q <= Q; ++q) {
+            if (lane == 0) SC_STAT(5, 1);
+            __syncwarp();
+            const int e = l - q;  // entry layer (-1: through the domain bottom)
+            if (act && e >= -1) {
+              const int hi = uprev;  // Uf(P[e + 1])
+              const int ue = e >= 0 ? Uf(P[e]) : 0;
+              uprev = ue;
+              const int lo = max(ue, uPlR);
+              // bottom -> right corners: the shortest is the lowest member (anchor lo)
+              int a1 = lo;
+              const int b1 = min(hi, uPuR);
+              if (a1 < b1) {
+                const double dbot = base + (double)a1 * dz + rho - Pl;
+                if ((float)dbot * ti < kScSliverGuard) {
+                  const int mphys = mz ? B - 1 - a1 : a1;
+                  const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
+                  if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) ++a1;
+                }
+                if (a1 < b1)
+                  cell.corner(a1, b1, r, lgR, ci, a1, (float)(base + (double)a1 * dz + rho - Pl), dzf, ti);
+              }
+              // bottom -> top (full axial, Eq. 11)
+              cell.full(max(lo, uPuR), hi, r, lgR, ci, (float)(Pu - Pl) * ti);
+            }
           }
         }
         // the cell's tally: sum over its R lanes, c_{a,n} * T -> FSR tally

@@ -18,9 +18,11 @@ import problems as P  # noqa: E402
 
 exp = "--exp" in sys.argv
 sched = next((int(a.split("=")[1]) for a in sys.argv if a.startswith("--schedule=")), 0)
-for cfg in [int(x) for x in sys.argv[1:] if not x.startswith("-")] or [4]:
+# extra solver options as key=value (e.g. sc_lanes_per_cell=1)
+extra = {a.split("=")[0]: int(a.split("=")[1]) for a in sys.argv[1:] if "=" in a and not a.startswith("-")}
+for cfg in [int(x) for x in sys.argv[1:] if not x.startswith("-") and "=" not in x] or [4]:
     torch.cuda.set_device(0)
-    s = M.Solver(M.Problem(P.config(cfg)), exp_mode=1 if exp else 0, schedule=sched)
+    s = M.Solver(M.Problem(P.config(cfg)), exp_mode=1 if exp else 0, schedule=sched, **extra)
     s.iterate(2)
     ms = []
     for _ in range(5):
@@ -28,7 +30,7 @@ for cfg in [int(x) for x in sys.argv[1:] if not x.startswith("-")] or [4]:
         ms.append(s.timings()["sweep_ms_last"])
     t = s.timings()
     med = float(np.median(ms))
-    print(json.dumps({"lib": os.path.basename(M.SO_PATH), "cfg": cfg, "exp": exp, "schedule": sched, "sweep_ms": med,
+    print(json.dumps({"lib": os.path.basename(M.SO_PATH), "cfg": cfg, "exp": exp, "schedule": sched, "opts": extra, "sweep_ms": med,
                       "integrations_per_s": t["n_integrations"] / (med * 1e-3),
                       "exp_fraction": t["exp_segments"] / max(1, t["n_segs3d"]),
                       "exp_gb": t["exp_bytes"] / 1e9, "setup_ms": t["setup_ms"]}), flush=True)
