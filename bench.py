@@ -8,8 +8,14 @@ inputs resident in HBM.  `value` = 3D-MOC segment-group integrations per second
 (2 x N_seg3D x G per iteration) over the whole job.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
+                    [--backend nccl|gloo] [--schedule 3]
 
-N > 1 is launched by torchrun (one rank per GPU, NCCL); rank 0 prints the line.
+N > 1: one rank per GPU.  Under torchrun (RANK/WORLD_SIZE set) each process is a rank; run
+directly with --gpus N > 1, bench.py re-launches itself through torch.distributed.run
+(127.0.0.1).  Backend nccl (default): the library owns an NCCL communicator and the whole
+iteration (sweep, tally all-reduce, boundary-psi halo, finalize) is one CUDA-graph replay;
+gloo (e.g. several ranks sharing one GPU for testing): the exchange is staged through host
+memory.  Rank 0 prints the line; `value` = all ranks' integrations / max-over-ranks time.
 `--impl reference` times the fp64 CPU oracle (oracle/) on the host cores on a
 bounded sample of the same workload (the oracle is a deliberately slow checker:
 the ratio is context, parity and roofline fraction are the headline).
@@ -181,24 +187,38 @@ def run_reference(args):
     return 0
 
 
+def relaunch(args) -> int:
+    """--gpus N > 1 without torchrun: run this script under torch.distributed.run."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def run_ours(args):
     import torch
 
     import paper_2503_17743_b200 as M
 
     rank, world, local = _dist_env()
+    ndev = torch.cuda.device_count()
+    backend = args.backend or ("nccl" if world <= ndev else "gloo")
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = local
+        dist.init_process_group(backend)
+    dev = local % max(1, ndev)  # gloo testing: several ranks may share one GPU
+    torch.cuda.set_device(dev)
     prob = P.config(args.config)
     t0 = time.time()
     pr = M.Problem(prob)
     t_lay = time.time() - t0
     st = pr.stats()
     t0 = time.time()
-    s = M.Solver(pr, device=dev, schedule=args.schedule, rank=rank, world=world, exp_mode=1 if args.exp else 0)
+    s = M.Solver(pr, device=dev, schedule=args.schedule, rank=rank, world=world, exp_mode=1 if args.exp else 0,
+                 backend=backend if world > 1 else None)
     t_setup = time.time() - t0
     tm = s.timings()
     G = pr.G
@@ -210,24 +230,31 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
-    # timed region: K full iterations, CUDA events on the solver's stream
-    sweep_ms = []
+    # timed region: K full iterations in one library call (each a CUDA-graph replay, no
+    # host synchronisation in between), CUDA events on the solver's stream
     with ClockSampler(dev) as clk:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
         e0.record(stream)
-        for _ in range(args.steps):
-            s.iterate(1)
-            sweep_ms.append(s.timings()["sweep_ms_last"])
+        s.iterate(args.steps)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         ms = e0.elapsed_time(e1)
+    rank_ms = [ms]
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ms], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        out = [None] * world
+        dist.all_gather_object(out, ms)
+        rank_ms = [float(x) for x in out]
+        ms = max(rank_ms)
+    # per-iteration sweep-kernel times (events around the sweep inside each replay)
+    sweep_ms = []
+    for _ in range(args.steps):
+        s.iterate(1)
+        sweep_ms.append(s.timings()["sweep_ms_last"])
     ms_step = ms / args.steps
     value = nint * args.steps / (ms * 1e-3)  # whole job (single problem, strong scaling)
     k, res = s.iterate(0)
@@ -269,6 +296,25 @@ def run_ours(args):
     achieved = nint_rank / (sweep_med * 1e-3)
     peak = r_alu(G, mhz_max)
     kerr = k_eff_errors(M, dev) if rank == 0 and not args.no_parity else None
+    # |k_gpu - k_oracle| on the benched configuration itself: the fp64 oracle's fixed-N
+    # golden (tools/oracle_golden.py, SURVEY §8(c) fixed-N parity), every rank iterating
+    gold = os.path.join(ROOT, "tests", "golden", f"cfg{args.config}_it{ {4: 5, 5: 2}.get(args.config, 0)}.npz")
+    bench_parity = None
+    if not args.no_parity and os.path.exists(gold):
+        g = np.load(gold)
+        s.reset()
+        kg, _ = s.iterate(int(g["fixed_iters"]))
+        phi = s.scalar_flux().reshape(-1)[g["sample_idx"]]
+        ref = g["phi_sample"]
+        pm = float(g["phi_max"])
+        mask = ref >= 1e-6 * pm
+        bench_parity = {"iterations": int(g["fixed_iters"]), "k_gpu": kg, "k_oracle": float(g["k"]),
+                        "abs_err": abs(kg - float(g["k"])),
+                        "flux_rel_max": float(np.max(np.abs(phi[mask] - ref[mask]) / ref[mask])),
+                        "flux_linf": float(np.max(np.abs(phi - ref)) / pm), "flux_elements_sampled": int(ref.size),
+                        "source": os.path.relpath(gold, ROOT)}
+    if kerr is not None:
+        kerr["benched_config_vs_oracle"] = bench_parity
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = oracle_sample(prob, target_s=args.ref_seconds)
@@ -276,7 +322,7 @@ def run_ours(args):
     # the unit that binds in practice (from the committed ncu --set full capture of this
     # kernel and config): the L1 LSU data pipe and the issue rate, next to R_ALU
     binding = None
-    np_ = os.path.join(ROOT, "profiles", f"ncu_sweep_cfg{args.config}_r1i.json")
+    np_ = os.path.join(ROOT, "profiles", f"ncu_sweep_cfg{args.config}_s{args.schedule}.json")
     if os.path.exists(np_):
         try:
             mt = json.load(open(np_))[0]["metrics"]
@@ -286,7 +332,7 @@ def run_ours(args):
         except Exception:
             binding = None
     traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}.json")
+    tp = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}_s{args.schedule}.json")
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
@@ -302,7 +348,10 @@ def run_ours(args):
                    "schedule": args.schedule, "k_eff_after": k, "residual_after": res,
                    "l2": "inputs larger than L2 (boundary psi %.1f GB)" % (2 * 2 * st["n_tracks3d"] * 8 * 4 / 1e9),
                    "host_laydown_s": round(t_lay, 2), "device_setup_s": round(t_setup, 2),
-                   "sweep_ms_median": sweep_med, "device_gb": round(tm["device_bytes"] / 1e9, 2)},
+                   "sweep_ms_median": sweep_med, "device_gb": round(tm["device_bytes"] / 1e9, 2),
+                   "emitted_last": emitted, "emitted_expected": 2 * tm["n_segs3d"] if world == 1 else None,
+                   "backend": backend if world > 1 else None, "per_rank_ms": rank_ms,
+                   "cuda_graph": True},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT, "frac": achieved / peak,
                      "traffic": traffic, "kernel": "k_sweep", "peak_basis":
                          f"R_ALU = 148 SM x {mhz_max:.0f} MHz ({kind} sm_max) x 128 / (5 + 5/G), SURVEY 8(d)",
@@ -311,7 +360,7 @@ def run_ours(args):
                      "measured_binding": binding},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "moc_solver_update_materials + moc_iterate(1) + moc_get_scalar_flux"},
-        "gpu_launches": tm["launches_per_iter"] * args.steps,
+        "gpu_launches": tm["launches_per_iter"] * args.steps,  # kernels in the K timed graph replays
         "clocks": clocks,
         "cpu_baseline": cpu,
         "k_eff_err": kerr,
@@ -331,7 +380,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--schedule", type=int, default=0)
+    ap.add_argument("--schedule", type=int, default=3)
+    ap.add_argument("--backend", default=None, choices=[None, "nccl", "gloo"],
+                    help="multi-rank exchange (default nccl when every rank has its own GPU, else gloo)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the closed-form k-eff error legs")
     ap.add_argument("--exp", action="store_true", help="EXP/OTF hybrid of §4.2 instead of pure OTF")
@@ -339,6 +390,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     return run_ours(args)
 
 

@@ -41,7 +41,9 @@ enum {
   MOC_E_NUMERIC = -9,     /* NaN / negative scalar flux                              */
   MOC_E_NOCONV = -10,     /* max_iter reached without convergence                    */
   MOC_E_CUDA = -11,       /* CUDA runtime error                                              */
-  MOC_E_NCCL = -12,       /* collective error                                                */
+  MOC_E_NCCL = -12,       /* multi-GPU exchange failed: NCCL could not be loaded (libnccl.so.2)
+                             or returned an error (message names the call and ncclResult), or
+                             the caller's exchange callback returned non-zero               */
   MOC_E_STATE = -13       /* call order (e.g. tracks not generated)                          */
 };
 
@@ -151,18 +153,43 @@ int moc_halo_plan(const moc_problem* p, int32_t world, const int32_t* owner, int
                   int64_t* slots, int64_t cap, int64_t* n);
 
 /* ---------------------------------------------------------------- solver */
+/* Multi-GPU: one process per GPU, `world` ranks.  Each rank sweeps its
+ * contiguous cost-balanced share of the z-stacks; every iteration the fp32 FSR tally
+ * [J][Gp] (+ the leakage in one tail element) is sum-all-reduced and the outgoing boundary
+ * psi of cut-crossing links is exchanged with the owning ranks.
+ *   backend MOC_COMM_NCCL: the library owns an NCCL communicator built from nccl_id
+ *     (rank 0 calls moc_nccl_unique_id and the caller broadcasts the 128 bytes, e.g. with
+ *     torch.distributed); the all-reduce and the grouped send/recv run on the solver's
+ *     stream inside moc_iterate / moc_solve, which then capture each iteration in a CUDA
+ *     graph (no host synchronisation between iterations).  NCCL is loaded at run time
+ *     (dlopen libnccl.so.2; torch has it in-process): no link dependency.
+ *   backend MOC_COMM_CALLER: the caller performs the exchange, either by driving
+ *     moc_iteration_sweep / moc_iteration_finish itself or by registering a host callback
+ *     with moc_solver_set_exchange (used with gloo on one GPU, for tests). */
+enum { MOC_COMM_CALLER = 0, MOC_COMM_NCCL = 1 };
 typedef struct {
   int32_t rank, world;      /* world == 1: single GPU                                 */
-  int32_t exchange_on_host; /* reserved (0)                                           */
+  int32_t backend;          /* MOC_COMM_CALLER or MOC_COMM_NCCL                       */
+  uint8_t nccl_id[128];     /* ncclUniqueId (backend MOC_COMM_NCCL), same on every rank */
 } moc_comm_desc;
 
+/* ncclGetUniqueId into id[128] (rank 0; MOC_E_NCCL if NCCL cannot be loaded). */
+int moc_nccl_unique_id(uint8_t* id);
+
+/* Sweep schedules.  MOC_SCHED_STACK_COLLECTIVE is the product path (opts == NULL selects
+ * it); the others are kept as measured baselines.  Schedule 0 accumulates the tally in a
+ * per-unit u32 fixed point and misses the per-element flux criterion at convergence in
+ * low-flux FSRs (2e-3 on the converged cfg3 assembly). */
+enum {
+  MOC_SCHED_TRACK_BANDS = 0,       /* persistent cost-sorted stack-band units, one thread per 3D track */
+  MOC_SCHED_ALG2 = 1,              /* Alg. 2 grid-stride over 3D tracks in Alg. 1 order (paper baseline) */
+  MOC_SCHED_SERPENTINE = 2,        /* Alg. 2 over tracks sorted by segment count + §4.3 serpentine */
+  MOC_SCHED_STACK_COLLECTIVE = 3   /* one warp per band of a z-stack, lanes own (2D segment, layer)
+                                      cells, exponentials shared per cell, register tallies:
+                                      P:68, Eqs. 6-11; SURVEY §8(f) NEXT-2 */
+};
 typedef struct {
-  int32_t schedule;     /* 0 = persistent cost-sorted stack-band units, one thread per 3D track,
-                           1 = Alg. 2 grid-stride over 3D tracks in Alg. 1 order (paper baseline),
-                           2 = Alg. 2 over tracks sorted by segment count with the §4.3 serpentine,
-                           3 = stack-collective sweep (one warp per band of a z-stack, lanes own
-                               (2D segment, layer) cells, exponentials shared per cell:
-                               P:68, Eqs. 6-11) */
+  int32_t schedule;     /* MOC_SCHED_* */
   int32_t threads, blocks;  /* Alg. 2 launch shape (P:146 default 512 x 512); 0 = default */
   int32_t deterministic;    /* reserved (0) */
   int32_t tile_cells;       /* schedule 0: cap on FSR cells per shared-memory tally chunk
@@ -176,6 +203,10 @@ typedef struct {
   int32_t sc_lanes_per_cell; /* schedule 3: lanes per (2D segment, layer) cell, 1/2/4/8 (0 = per stack) */
   int32_t sc_psi_cap;        /* schedule 3: boundary-psi band capacity per warp in members (0 = fill
                                 the shared memory of kScMinBlocks CTAs per SM) */
+  int32_t v2_lane_stride;    /* schedule 0: force the member stride between the lanes of a warp to
+                                1, 2, 4 or 8 (0 = per unit from the stack's dz; for tests) */
+  int32_t no_graph;          /* 1: launch every iteration's kernels individually instead of
+                                replaying a captured CUDA graph (debugging / A-B) */
 } moc_solver_opts;
 
 /* Upload the laydown to `device`, allocate HBM state (boundary psi double buffer,
@@ -192,10 +223,12 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
 int moc_solver_destroy(moc_solver* s);
 const char* moc_solver_last_error(const moc_solver* s);
 
-/* Run n_iter power iterations (A3..A7 on the device; A8 is driven by the caller through
- * moc_solver_comm_buffers when world > 1).  Initial state phi = 1, k = 1, psi = 0 (Q11).
- * Writes the final k and fission-source residual. Stream-ordered; synchronises the
- * stream once at the end to read k (16 bytes D2H). */
+/* Run n_iter power iterations (A3..A8 on the device).  Initial state phi = 1, k = 1,
+ * psi = 0 (Q11).  world > 1 needs backend MOC_COMM_NCCL or a registered exchange callback
+ * (else MOC_E_STATE).  Each iteration is one CUDA-graph replay (captured on first use per
+ * Jacobi buffer parity) unless opts.no_graph or a host callback is involved.  Writes the
+ * final k and fission-source residual; synchronises the stream once at the end to read
+ * them (16 bytes D2H). */
 int moc_iterate(moc_solver* s, int32_t n_iter, double* k_out, double* residual_out);
 
 typedef struct { double tol_k, tol_src; int32_t max_iter, check_every; } moc_solve_opts;
@@ -212,7 +245,10 @@ int moc_solver_update_materials(moc_solver* s, const double* sigma_t, const doub
 
 /* Results (host, caller-owned). phi [J][G] normalised to sum_j V_j F_j = 1. */
 int moc_get_scalar_flux(moc_solver* s, double* phi);
-int moc_get_fsr_volumes(moc_solver* s, double* vol);
+/* FSR volumes [J] (cm^3): vol_track = the track estimate V_j = sum_{a,n} W_{a,n}/(2 pi)
+ * A_perp sum L over every 3D segment in j (App. A.5, device walk); vol_analytic = ring /
+ * moderator area x layer height.  Either pointer may be NULL (not both). */
+int moc_get_fsr_volumes(moc_solver* s, double* vol_track, double* vol_analytic);
 int moc_get_history(moc_solver* s, double* k_hist, double* res_hist, int32_t cap, int32_t* n);
 int moc_get_balance(moc_solver* s, double* production, double* absorption, double* leakage);
 
@@ -267,6 +303,13 @@ int moc_solver_halo_counts(moc_solver* s, int64_t* send_elems, int64_t* recv_ele
  * caller's allreduce of the tally / halo exchange, finish (A7). */
 int moc_iteration_sweep(moc_solver* s);
 int moc_iteration_finish(moc_solver* s);
+
+/* Backend MOC_COMM_CALLER with world > 1: host callback that performs the exchange on the
+ * buffers of moc_solver_comm_buffers (the stream is synchronised before the call); with it
+ * registered, moc_iterate / moc_solve run multi-rank.  Return 0 on success (else the
+ * iteration fails with MOC_E_NCCL).  fn == NULL unregisters. */
+typedef int (*moc_exchange_fn)(void* ctx);
+int moc_solver_set_exchange(moc_solver* s, moc_exchange_fn fn, void* ctx);
 
 #ifdef __cplusplus
 }

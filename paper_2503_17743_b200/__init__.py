@@ -53,15 +53,21 @@ class moc_track_stats(C.Structure):
                                          "n_cycles", "n_segs3d_raw")]
 
 
+MOC_COMM_CALLER, MOC_COMM_NCCL = 0, 1
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p)
+
+
 class moc_comm_desc(C.Structure):
-    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("exchange_on_host", C.c_int32)]
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("backend", C.c_int32),
+                ("nccl_id", C.c_uint8 * 128)]
 
 
 class moc_solver_opts(C.Structure):
     _fields_ = [("schedule", C.c_int32), ("threads", C.c_int32), ("blocks", C.c_int32),
                 ("deterministic", C.c_int32), ("tile_cells", C.c_int32), ("exp_mode", C.c_int32),
                 ("exp_budget_mb", C.c_int32), ("exp_fraction", C.c_double),
-                ("sc_lanes_per_cell", C.c_int32), ("sc_psi_cap", C.c_int32)]
+                ("sc_lanes_per_cell", C.c_int32), ("sc_psi_cap", C.c_int32), ("v2_lane_stride", C.c_int32),
+                ("no_graph", C.c_int32)]
 
 
 class moc_solve_opts(C.Structure):
@@ -120,7 +126,7 @@ SIGNATURES = {
     "moc_reset": (C.c_int, [_vp]),
     "moc_solver_update_materials": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
     "moc_get_scalar_flux": (C.c_int, [_vp, _vp]),
-    "moc_get_fsr_volumes": (C.c_int, [_vp, _vp]),
+    "moc_get_fsr_volumes": (C.c_int, [_vp, _vp, _vp]),
     "moc_get_history": (C.c_int, [_vp, _vp, _vp, _i32, _P(_i32)]),
     "moc_get_balance": (C.c_int, [_vp, _P(_d), _P(_d), _P(_d)]),
     "moc_device_trace_checksums": (C.c_int, [_vp, _i64, _i64, _vp, _vp, _vp]),
@@ -130,6 +136,8 @@ SIGNATURES = {
     "moc_attenuation_probe": (C.c_int, [C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "moc_sweep_checksums": (C.c_int, [_vp, _vp, _vp]),
     "moc_iteration_sweep": (C.c_int, [_vp]),
+    "moc_nccl_unique_id": (C.c_int, [_vp]),
+    "moc_solver_set_exchange": (C.c_int, [_vp, EXCHANGE_FN, _vp]),
     "moc_iteration_finish": (C.c_int, [_vp]),
 }
 # host-only test hook (not in the public header): backward OTF walk of one track
@@ -324,13 +332,18 @@ class _DeviceArray:
 class Solver:
     """Device state + power iteration on one GPU (one rank)."""
 
-    def __init__(self, problem: Problem, device: int = 0, stream=None, schedule: int = 0, threads: int = 0,
+    def __init__(self, problem: Problem, device: int = 0, stream=None, schedule: int = 3, threads: int = 0,
                  blocks: int = 0, rank: int = 0, world: int = 1, tile_cells: int = 0, exp_mode: int = 0,
                  exp_budget_mb: int = 0, exp_fraction: float = 0.0, sc_lanes_per_cell: int = 0,
-                 sc_psi_cap: int = 0):
+                 sc_psi_cap: int = 0, v2_lane_stride: int = 0, no_graph: bool = False, backend: str | None = None):
+        """world > 1: one rank of a torch.distributed job.  backend "nccl"
+        (default when the process group is NCCL): the library owns an NCCL communicator
+        and runs the whole iteration on the device; "gloo": the exchange is staged through
+        host memory by a Python callback (tests, several ranks on one GPU)."""
         L = lib()
         self.problem = problem
         self._h = C.c_void_p()
+        self._xfn = None
         if stream is None:
             try:
                 import torch
@@ -338,8 +351,20 @@ class Solver:
             except Exception:  # torch without CUDA: legacy default stream
                 stream = 0
         opts = moc_solver_opts(schedule, threads, blocks, 0, tile_cells, exp_mode, exp_budget_mb, exp_fraction,
-                               sc_lanes_per_cell, sc_psi_cap)
-        comm = moc_comm_desc(rank, world, 0)
+                               sc_lanes_per_cell, sc_psi_cap, v2_lane_stride, int(bool(no_graph)))
+        comm = moc_comm_desc(rank, world, MOC_COMM_CALLER)
+        if world > 1:
+            import torch.distributed as dist
+            backend = backend or ("nccl" if dist.get_backend() == "nccl" else "gloo")
+            if backend == "nccl":
+                comm.backend = MOC_COMM_NCCL
+                uid = (C.c_uint8 * 128)()
+                if rank == 0:
+                    _check(L.moc_nccl_unique_id(uid), None, None)
+                obj = [bytes(uid)]
+                dist.broadcast_object_list(obj, src=0)
+                C.memmove(comm.nccl_id, obj[0], 128)
+        self.backend = backend if world > 1 else None
         rc = L.moc_solver_create(C.byref(self._h), problem.handle, device, C.c_void_p(stream), C.byref(comm),
                                  C.byref(opts))
         if rc != MOC_OK:
@@ -348,6 +373,30 @@ class Solver:
         self.J = problem.num_fsrs()
         self.world, self.rank, self.device = world, rank, device
         self._comm = None
+        if world > 1 and self.backend != "nccl":
+            self._xfn = EXCHANGE_FN(self._host_exchange)
+            self._call(L.moc_solver_set_exchange, self._xfn, None)
+
+    def _host_exchange(self, _ctx):
+        """Exchange callback (backend gloo): sum all-reduce of the tally and all-to-all of
+        the cut-crossing boundary psi, staged through host memory.  Every rank takes part
+        in both collectives every iteration (an empty halo still participates)."""
+        try:
+            import torch.distributed as dist
+            c = self._comm_tensors()
+            t = c["tally"].cpu()
+            dist.all_reduce(t)
+            c["tally"].copy_(t)
+            rbuf = c["recv"].cpu()
+            dist.all_to_all_single(rbuf, c["send"].cpu(), c["recv_splits"], c["send_splits"])
+            c["recv"].copy_(rbuf)
+            import torch
+            torch.cuda.current_stream(self.device).synchronize()
+            return 0
+        except Exception:  # reported by the library as MOC_E_NCCL
+            import traceback
+            traceback.print_exc()
+            return 1
 
     def _comm_tensors(self):
         """torch views (via __cuda_array_interface__) of the library's tally and halo
@@ -382,31 +431,32 @@ class Solver:
         self.__del__()
 
     def iterate(self, n: int):
+        """n power iterations (multi-rank: the exchange runs inside the library)."""
         k, r = C.c_double(), C.c_double()
-        if self.world > 1:
-            # A3-A6 on the device, NCCL sum of the tally + boundary-psi halo all-to-all on
-            # torch's current stream (= the solver's stream), then A7 on the device.
-            import torch.distributed as dist
-            c = self._comm_tensors()
-            host = dist.get_backend() != "nccl"  # gloo (tests): stage through host memory
-            for _ in range(int(n)):
-                self._call(lib().moc_iteration_sweep)
-                # both collectives are called on every rank every iteration (a rank with an
-                # empty halo still takes part, or the others would wait forever)
-                if host:
-                    t = c["tally"].cpu()
-                    dist.all_reduce(t)
-                    c["tally"].copy_(t)
-                    rbuf = c["recv"].cpu()
-                    dist.all_to_all_single(rbuf, c["send"].cpu(), c["recv_splits"], c["send_splits"])
-                    c["recv"].copy_(rbuf)
-                else:
-                    dist.all_reduce(c["tally"])
-                    dist.all_to_all_single(c["recv"], c["send"], c["recv_splits"], c["send_splits"])
-                self._call(lib().moc_iteration_finish)
-            n = 0
         self._call(lib().moc_iterate, int(n), C.byref(k), C.byref(r))
         return k.value, r.value
+
+    def iterate_split(self, n: int):
+        """Caller-driven multi-rank iteration (moc_iteration_sweep / _finish with the
+        collectives issued from Python on torch's stream); the reference for the in-library
+        exchange in tests."""
+        import torch.distributed as dist
+        c = self._comm_tensors()
+        host = dist.get_backend() != "nccl"
+        for _ in range(int(n)):
+            self._call(lib().moc_iteration_sweep)
+            if host:
+                t = c["tally"].cpu()
+                dist.all_reduce(t)
+                c["tally"].copy_(t)
+                rbuf = c["recv"].cpu()
+                dist.all_to_all_single(rbuf, c["send"].cpu(), c["recv_splits"], c["send_splits"])
+                c["recv"].copy_(rbuf)
+            else:
+                dist.all_reduce(c["tally"])
+                dist.all_to_all_single(c["recv"], c["send"], c["recv_splits"], c["send_splits"])
+            self._call(lib().moc_iteration_finish)
+        return self.iterate(0)
 
     def solve(self, tol_k=1e-7, tol_src=1e-6, max_iter=5000, check_every=10):
         o = moc_solve_opts(tol_k, tol_src, max_iter, check_every)
@@ -427,10 +477,16 @@ class Solver:
         self._call(lib().moc_get_scalar_flux, _p(phi))
         return phi
 
-    def fsr_volumes(self) -> np.ndarray:
+    def fsr_volumes(self, analytic: bool = False):
+        """Track-estimated FSR volumes [J]; with analytic=True also the analytic ones
+         as a second array."""
         v = np.zeros(self.J)
-        self._call(lib().moc_get_fsr_volumes, _p(v))
-        return v
+        if not analytic:
+            self._call(lib().moc_get_fsr_volumes, _p(v), None)
+            return v
+        va = np.zeros(self.J)
+        self._call(lib().moc_get_fsr_volumes, _p(v), _p(va))
+        return v, va
 
     def history(self):
         n = C.c_int32()

@@ -20,6 +20,19 @@ HEADERS = ["host.h", "otf.h", "sweep_v2.cuh", "sweep_sc.cuh"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 
+def _nccl_include() -> str:
+    """nccl.h for types/prototypes (NCCL itself is dlopen'ed at run time): the pip
+    nvidia-nccl headers matching torch's bundled libnccl.so.2, else the system ones."""
+    try:
+        import nvidia.nccl
+        d = os.path.join(list(nvidia.nccl.__path__)[0], "include")
+        if os.path.exists(os.path.join(d, "nccl.h")):
+            return d
+    except ImportError:
+        pass
+    return "/usr/include"
+
+
 def _stale() -> bool:
     if not os.path.exists(SO):
         return True
@@ -36,10 +49,11 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
     tmp = target + ".tmp"
-    cmd = [nvcc, ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-shared", "-o", tmp] + [f"-D{d}" for d in defines] + [
+    cmd = [nvcc, ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-shared", "-o", tmp,
+           "-I", _nccl_include()] + [f"-D{d}" for d in defines] + [
            "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off,-fno-fast-math",
            "-Xptxas", "-v" if verbose else "-O3",
-           "-lgomp"] + [os.path.join(CSRC, f) for f in SOURCES]
+           "-lgomp", "-ldl"] + [os.path.join(CSRC, f) for f in SOURCES]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd, cwd=HERE)

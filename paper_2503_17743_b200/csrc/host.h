@@ -51,6 +51,7 @@ struct Geometry {
 
   int64_t region_at(int cx, int cy, double x, double y) const;  // ring test inside cell (cx, cy)
   int mat_of_fsr(int64_t j) const;
+  void analytic_volumes(double* vol) const;  // [n_fsr]
 };
 
 struct Laydown {

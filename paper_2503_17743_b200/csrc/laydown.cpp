@@ -146,6 +146,29 @@ int64_t Geometry::region_at(int cx, int cy, double x, double y) const {
   return prefix[c] + local;
 }
 
+// Analytic FSR volumes (S:83-85 'analytic_volume'): ring q of a cell is the annulus
+// pi (r_q^2 - r_{q-1}^2), the moderator the cell minus the outer circle, times the layer
+// height (rings lie inside their cell; App. A.6 numbering j = r * NL + layer).
+void Geometry::analytic_volumes(double* vol) const {
+  const double pi = 3.14159265358979323846;
+  for (int c = 0; c < nx * ny; ++c) {
+    const int ty = cell_type[c], nr = n_rings[ty];
+    double prev = 0.0;
+    for (int q = 0; q <= nr; ++q) {
+      double area;
+      if (q < nr) {
+        const double rq = radii[(size_t)ty * max_rings + q];
+        area = pi * (rq * rq - prev * prev);
+        prev = rq;
+      } else {
+        area = px * py - pi * prev * prev;
+      }
+      const int64_t r = prefix[c] + q;
+      for (int l = 0; l < NL; ++l) vol[r * NL + l] = area * (planes[l + 1] - planes[l]);
+    }
+  }
+}
+
 int Geometry::mat_of_fsr(int64_t j) const {
   int64_t r = j / NL;
   int l = (int)(j % NL);

@@ -11,6 +11,8 @@
 //   boundary psi  psi f32[2][2*T3][GP]  (Jacobi double buffer, lazily normalised)
 //   FSR arrays    mat u8[J], qt f32[J][GP], phi f32[J][GP], tally f64[J][GP], vol f64[J]
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types and prototypes only: NCCL is loaded at run time (nccl_api below)
 #include <thrust/device_ptr.h>
 #include <thrust/execution_policy.h>
 #include <thrust/sequence.h>
@@ -472,6 +474,61 @@ T* dmalloc(size_t n, int64_t& bytes) {
   return p;
 }
 
+// NCCL loaded at run time (dlopen libnccl.so.2): the single-GPU library has no NCCL link
+// dependency, and in a torch process the already-loaded copy is reused.
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+};
+
+NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return a;
+    }
+#define MOC_SYM(f, name)                                      \
+  a.f = reinterpret_cast<decltype(a.f)>(dlsym(h, name));     \
+  if (!a.f) {                                                 \
+    a.why = std::string("libnccl.so.2 lacks ") + name;        \
+    return a;                                                 \
+  }
+    MOC_SYM(getUniqueId, "ncclGetUniqueId")
+    MOC_SYM(commInitRank, "ncclCommInitRank")
+    MOC_SYM(commDestroy, "ncclCommDestroy")
+    MOC_SYM(allReduce, "ncclAllReduce")
+    MOC_SYM(send, "ncclSend")
+    MOC_SYM(recv, "ncclRecv")
+    MOC_SYM(groupStart, "ncclGroupStart")
+    MOC_SYM(groupEnd, "ncclGroupEnd")
+    MOC_SYM(errorString, "ncclGetErrorString")
+#undef MOC_SYM
+    a.ok = true;
+    return a;
+  }();
+  if (!api.ok) throw Error(MOC_E_NCCL, api.why);
+  return api;
+}
+
+#define NCCL_OK(call)                                                                           \
+  do {                                                                                          \
+    ncclResult_t r_ = (call);                                                                   \
+    if (r_ != ncclSuccess)                                                                      \
+      throw Error(MOC_E_NCCL, std::string(#call) + ": " + nccl_api().errorString(r_));        \
+  } while (0)
+
 }  // namespace
 
 struct moc_solver {
@@ -517,6 +574,7 @@ struct moc_solver {
   bool sweep_timed = false;
   std::vector<double> sigma_t, nusf, sigs;  // host copies (balance)
   std::vector<int32_t> mat_host;
+  std::vector<double> vol_analytic;  // S:83-85, host copy
   float* h_xs = nullptr;  // pinned staging for cross-section uploads
   int64_t xs_bytes = 0;
   // v2 (schedule 0): persistent stack-band units
@@ -548,6 +606,11 @@ struct moc_solver {
   float *d_halo_send = nullptr, *d_halo_recv = nullptr;
   std::vector<int64_t> send_counts, recv_counts;  // per peer, in slots
   double owned_cost = 0;
+  ncclComm_t nccl = nullptr;        // backend MOC_COMM_NCCL: library-owned communicator
+  moc_exchange_fn xfn = nullptr;    // backend MOC_COMM_CALLER: host exchange callback
+  void* xctx = nullptr;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};  // one iteration, per Jacobi buffer parity
+  cudaStream_t cap_stream = nullptr;  // private non-blocking stream the graphs are captured on
 };
 
 namespace {
@@ -709,6 +772,15 @@ void v2_configure(moc_solver* s) {
   s->sweep_threads = kV2Threads;
 }
 
+// an event record that is also an event-record node when the stream is being captured
+// into the iteration's CUDA graph (so every replay re-times the sweep)
+void record_event(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CUDA_OK(cudaStreamIsCapturing(st, &cs));
+  if (cs == cudaStreamCaptureStatusActive) CUDA_OK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+  else CUDA_OK(cudaEventRecord(e, st));
+}
+
 // first half of an iteration: A3 source, A4-A6 sweep of this rank's units; for world > 1
 // also gathers the halo (outgoing psi of cut-crossing links) and parks the leakage in the
 // tally's tail so one all-reduce carries both.
@@ -729,10 +801,10 @@ void iter_sweep_half(moc_solver* s, bool time_it) {
   } else {
     CUDA_OK(cudaMemsetAsync(s->d_tally, 0, sizeof(double) * s->J * s->GP, s->stream));
   }
-  if (time_it) CUDA_OK(cudaEventRecord(s->ev[0], s->stream));
+  if (time_it) record_event(s->ev[0], s->stream);
   run_sweep<G, GP>(s);
   if (time_it) {
-    CUDA_OK(cudaEventRecord(s->ev[1], s->stream));
+    record_event(s->ev[1], s->stream);
     s->sweep_timed = true;
   }
   if (s->comm.world > 1) {
@@ -767,10 +839,42 @@ void iter_finish_half(moc_solver* s) {
   CUDA_OK(cudaGetLastError());
 }
 
+// A8 between the halves: sum all-reduce of the fp32 tally (+ the leakage in
+// its tail) and the grouped point-to-point exchange of cut-crossing boundary psi, on the
+// solver's stream (NCCL), or through the caller's host callback.
+void exchange(moc_solver* s) {
+  if (s->comm.world <= 1) return;
+  if (s->nccl) {
+    NcclApi& n = nccl_api();
+    const int GP = s->GP;
+    NCCL_OK(n.groupStart());
+    NCCL_OK(n.allReduce(s->d_tally32, s->d_tally32, (size_t)s->J * GP + 1, ncclFloat32, ncclSum, s->nccl,
+                        s->stream));
+    int64_t so = 0, ro = 0;
+    for (int p = 0; p < s->comm.world; ++p) {
+      if (s->send_counts[p])
+        NCCL_OK(n.send(s->d_halo_send + so * GP, (size_t)(s->send_counts[p] * GP), ncclFloat32, p, s->nccl,
+                       s->stream));
+      if (s->recv_counts[p])
+        NCCL_OK(n.recv(s->d_halo_recv + ro * GP, (size_t)(s->recv_counts[p] * GP), ncclFloat32, p, s->nccl,
+                       s->stream));
+      so += s->send_counts[p];
+      ro += s->recv_counts[p];
+    }
+    NCCL_OK(n.groupEnd());
+  } else if (s->xfn) {
+    CUDA_OK(cudaStreamSynchronize(s->stream));
+    if (s->xfn(s->xctx) != 0) throw Error(MOC_E_NCCL, "exchange callback failed");
+  } else {
+    throw Error(MOC_E_STATE, "world > 1 needs backend MOC_COMM_NCCL, an exchange callback, or "
+                             "moc_iteration_sweep/finish driven by the caller");
+  }
+}
+
 template <int G, int GP>
 void run_iteration(moc_solver* s, bool time_it) {
-  if (s->comm.world > 1) throw Error(MOC_E_STATE, "world > 1: drive iterations with moc_iteration_sweep/finish");
   iter_sweep_half<G, GP>(s, time_it);
+  exchange(s);
   iter_finish_half<G, GP>(s);
 }
 
@@ -969,7 +1073,57 @@ void destroy(moc_solver* s) {
     if (e) cudaEventDestroy(e);
   if (s->h_xs) cudaFreeHost(s->h_xs);
   if (s->h_planes) cudaFreeHost(s->h_planes);
+  for (auto& g : s->gexec)
+    if (g) cudaGraphExecDestroy(g);
+  if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  if (s->nccl) nccl_api().commDestroy(s->nccl);
   if (const_owner(s->device) == s->uid) const_owner(s->device) = 0;
+}
+
+// One power iteration: a replay of the captured graph of this Jacobi parity (captured on
+// first use: source, sweep, exchange, finalize, k, normalisation, residual), or direct
+// launches when graphs are off or the exchange needs the host.
+void iterate_once(moc_solver* s, iter_fn f, bool time_it) {
+  const bool graph = !s->opts.no_graph && (s->comm.world <= 1 || s->nccl);
+  if (!graph) {
+    f(s, time_it);
+    return;
+  }
+  ensure_constants(s);  // outside the capture: the graph reads the constant bank as it is
+  const int c = s->cur;
+  if (!s->gexec[c]) {
+    // captured on a private non-blocking stream (the caller's may be the legacy default
+    // stream, which cannot be captured), replayed on the caller's stream
+    if (!s->cap_stream) CUDA_OK(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t user = s->stream;
+    cudaGraph_t g = nullptr;
+    CUDA_OK(cudaStreamSynchronize(user));
+    s->stream = s->cap_stream;
+    try {
+      CUDA_OK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        f(s, true);  // sweep timed by event-record nodes in every replay
+      } catch (...) {
+        cudaStreamEndCapture(s->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      CUDA_OK(cudaStreamEndCapture(s->stream, &g));
+    } catch (...) {
+      s->stream = user;
+      s->cur = c;
+      (void)cudaGetLastError();
+      throw;
+    }
+    s->stream = user;
+    s->cur = c;  // capture recorded the launches without running them
+    const cudaError_t e = cudaGraphInstantiate(&s->gexec[c], g, 0);
+    cudaGraphDestroy(g);
+    CUDA_OK(e);
+  }
+  CUDA_OK(cudaGraphLaunch(s->gexec[c], s->stream));
+  s->sweep_timed = true;
+  s->cur = 1 - c;
 }
 
 }  // namespace
@@ -1009,6 +1163,7 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     for (size_t i = 0; i < g.material.size(); ++i)
       if (g.material[i] >= mt.n_mat) throw Error(MOC_E_REFERENCE, "unknown material index");
     if (opts) s->opts = *opts;
+    else s->opts.schedule = MOC_SCHED_STACK_COLLECTIVE;  // the product sweep
     if (comm) s->comm = *comm;
     s->device = device;
     static std::atomic<uint64_t> next_uid{1};
@@ -1136,10 +1291,20 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
         upload(rr.data(), s->d_recv_slots, 4 * rr.size(), st);
         s->d_halo_send = dmalloc<float>(ss.size() * s->GP, B);
         s->d_halo_recv = dmalloc<float>(rr.size() * s->GP, B);
+        if (s->comm.backend == MOC_COMM_NCCL) {
+          static_assert(sizeof(ncclUniqueId) == sizeof(s->comm.nccl_id), "ncclUniqueId size");
+          ncclUniqueId id;
+          std::memcpy(&id, s->comm.nccl_id, sizeof(id));
+          NCCL_OK(nccl_api().commInitRank(&s->nccl, s->comm.world, id, s->comm.rank));
+        } else if (s->comm.backend != MOC_COMM_CALLER) {
+          throw Error(MOC_E_INVALID_ARG, "unknown comm backend");
+        }
       }
       CUDA_OK(cudaStreamSynchronize(st));
     }
     // --- FSR arrays and materials
+    s->vol_analytic.resize(s->J);
+    g.analytic_volumes(s->vol_analytic.data());
     s->mat_host.resize(s->J);
     std::vector<uint8_t> m8(s->J);
     for (int64_t j = 0; j < s->J; ++j) {
@@ -1230,13 +1395,10 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       {
         double hmin = 1e300;
         for (int l = 0; l < g.NL; ++l) hmin = std::min(hmin, g.planes[l + 1] - g.planes[l]);
-        const char* dv = std::getenv("MOC_V2_LANE_DIV");  // A/B override of the 1/3
-        s->h_lane = hmin / (dv ? std::atof(dv) : 3.0);
-        if (const char* e = std::getenv("MOC_V2_INTERLEAVE")) s->interleave = std::max(1, std::min(8, std::atoi(e)));
-        if (const char* e = std::getenv("MOC_V2_LANE_STRIDE")) {  // A/B override
-          const int v = std::atoi(e);
-          s->lane_lg = v >= 8 ? 3 : v >= 4 ? 2 : v >= 2 ? 1 : 0;
-        }
+        s->h_lane = hmin / 3.0;
+        const int v = s->opts.v2_lane_stride;
+        if (v != 0 && v != 1 && v != 2 && v != 4 && v != 8) throw Error(MOC_E_PARAM, "v2_lane_stride must be 0, 1, 2, 4 or 8");
+        if (v > 0) s->lane_lg = v == 8 ? 3 : v == 4 ? 2 : v == 2 ? 1 : 0;
       }
       std::vector<Unit> units;
       for (int64_t q = 0; q < s->S; ++q) {
@@ -1383,7 +1545,7 @@ int moc_iterate(moc_solver* s, int32_t n_iter, double* k_out, double* residual_o
     for (int it = 0; it < n_iter; ++it) {
       bool last = it == n_iter - 1;
       if (last) CUDA_OK(cudaEventRecord(s->ev[2], s->stream));
-      f(s, last);
+      iterate_once(s, f, last);
       if (last) CUDA_OK(cudaEventRecord(s->ev[3], s->stream));
     }
     double sc[SC_N];
@@ -1411,7 +1573,7 @@ int moc_solve(moc_solver* s, const moc_solve_opts* o, moc_result* r) {
     r->converged = 0;
     while (done < o->max_iter) {
       int n = std::min(every, o->max_iter - done);
-      for (int it = 0; it < n; ++it) f(s, false);
+      for (int it = 0; it < n; ++it) iterate_once(s, f, false);
       done += n;
       double sc[SC_N];
       read_scalars(s, sc);
@@ -1461,12 +1623,15 @@ int moc_get_scalar_flux(moc_solver* s, double* phi) {
   })
 }
 
-int moc_get_fsr_volumes(moc_solver* s, double* vol) {
-  if (!s || !vol) return MOC_E_INVALID_ARG;
+int moc_get_fsr_volumes(moc_solver* s, double* vol_track, double* vol_analytic) {
+  if (!s || (!vol_track && !vol_analytic)) return MOC_E_INVALID_ARG;
   SOLVER_TRY(s, {
-    CUDA_OK(cudaSetDevice(s->device));
-    CUDA_OK(cudaMemcpyAsync(vol, s->d_vol, 8 * s->J, cudaMemcpyDeviceToHost, s->stream));
-    CUDA_OK(cudaStreamSynchronize(s->stream));
+    if (vol_track) {
+      CUDA_OK(cudaSetDevice(s->device));
+      CUDA_OK(cudaMemcpyAsync(vol_track, s->d_vol, 8 * s->J, cudaMemcpyDeviceToHost, s->stream));
+      CUDA_OK(cudaStreamSynchronize(s->stream));
+    }
+    if (vol_analytic) std::memcpy(vol_analytic, s->vol_analytic.data(), 8 * (size_t)s->J);
   })
 }
 
@@ -1494,7 +1659,7 @@ int moc_get_balance(moc_solver* s, double* production, double* absorption, doubl
     std::vector<double> phi((size_t)s->J * s->G), vol(s->J);
     int rc = moc_get_scalar_flux(s, phi.data());
     if (rc) throw Error(rc, s->err);
-    rc = moc_get_fsr_volumes(s, vol.data());
+    rc = moc_get_fsr_volumes(s, vol.data(), nullptr);
     if (rc) throw Error(rc, s->err);
     double sc[SC_N];
     read_scalars(s, sc);
@@ -1655,6 +1820,25 @@ int moc_solver_halo_counts(moc_solver* s, int64_t* send_elems, int64_t* recv_ele
     send_elems[p] = p < (int)s->send_counts.size() ? s->send_counts[p] * s->GP : 0;
     recv_elems[p] = p < (int)s->recv_counts.size() ? s->recv_counts[p] * s->GP : 0;
   }
+  return MOC_OK;
+}
+
+int moc_nccl_unique_id(uint8_t* id) {
+  if (!id) return MOC_E_INVALID_ARG;
+  try {
+    ncclUniqueId u;
+    NCCL_OK(nccl_api().getUniqueId(&u));
+    std::memcpy(id, &u, sizeof(u));
+  } catch (const Error& e) {
+    return e.code;
+  }
+  return MOC_OK;
+}
+
+int moc_solver_set_exchange(moc_solver* s, moc_exchange_fn fn, void* ctx) {
+  if (!s) return MOC_E_INVALID_ARG;
+  s->xfn = fn;
+  s->xctx = ctx;
   return MOC_OK;
 }
 

@@ -1,15 +1,25 @@
 """GPU parity: the CUDA path through the C ABI against the fp64 oracle.
 
-Tolerances (north_star): k-eff within 1e-5 absolute; FSR scalar flux within 1e-4
-relative in the normalised L-infinity sense (max |phi_gpu - phi_or| / max phi_or,
-both normalised to sum V F = 1); track/segment counts and FSR ids bit-exact.
+Tolerances (north_star, SURVEY §8(c) 'Parity checks'): k-eff within 1e-5 absolute; FSR
+scalar flux within 1e-4 per element, max_{j,g} |phi_gpu - phi_or| / phi_or over the
+elements with phi_or >= 1e-6 max phi_or, and within 1e-4 in the max-normalised L-inf
+sense, both normalised to sum V F = 1 (reading Q12); track/segment counts and FSR ids
+bit-exact.  Every check is recorded (parity_log -> gpurun_out/parity_r2.json).
+
+Large cases compare against goldens written by tools/oracle_golden.py (which calls only
+oracle/): phi at a seeded sample of (FSR, group) elements plus the global max.
 """
+import os
+
 import numpy as np
 import pytest
 
 import problems as P
 
 pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TOL_K, TOL_PHI = 1e-5, 1e-4
 
 
 @pytest.fixture(scope="module")
@@ -24,69 +34,86 @@ def M():
 
 def _check_emitted(s):
     """Integrity counter: every merged 3D segment was applied exactly once per direction
-    in the last sweep (no lost or phantom emissions at chunk boundaries)."""
+    in the last sweep (no lost or phantom emissions at chunk / column boundaries)."""
     t = s.timings()
     assert t["emitted_last"] == 2 * t["n_segs3d"], (t["emitted_last"], t["n_segs3d"])
 
 
-def _flux_err(phi, ref):
-    linf = np.abs(phi - ref).max() / np.abs(ref).max()
-    mask = ref >= 1e-6 * ref.max()
-    rel = np.max(np.abs(phi[mask] - ref[mask]) / ref[mask])
+def _errors(phi, ref, phimax=None):
+    phimax = np.abs(ref).max() if phimax is None else phimax
+    linf = float(np.abs(phi - ref).max() / phimax)
+    mask = ref >= 1e-6 * phimax
+    rel = float(np.max(np.abs(phi[mask] - ref[mask]) / ref[mask]))
     return linf, rel
 
 
+def _check(log, case, k, k_ref, phi, ref, phimax=None, **extra):
+    """k within 1e-5; flux per element and normalised L-inf within 1e-4; recorded."""
+    linf, rel = _errors(np.asarray(phi), np.asarray(ref), phimax)
+    log.append(dict(case=case, k_gpu=float(k), k_oracle=float(k_ref), k_abs_err=abs(float(k) - float(k_ref)),
+                    flux_linf=linf, flux_rel_max=rel, **extra))
+    assert abs(k - k_ref) < TOL_K, (case, k, k_ref)
+    assert linf < TOL_PHI and rel < TOL_PHI, (case, linf, rel)
+
+
+def _golden(name):
+    return np.load(os.path.join(GOLD, name + ".npz"))
+
+
 def test_cfg1_k_inf(M, oracle_mod):
-    prob = P.config(1)
-    s = M.Solver(M.Problem(prob))
-    r = s.solve(tol_k=1e-9, tol_src=1e-8, max_iter=2000, check_every=5)
-    assert r["converged"]
-    assert r["k"] == pytest.approx(1.5, abs=1e-5)
-    phi = s.scalar_flux()
-    assert np.ptp(phi) / phi.mean() < 1e-5
+    for sched in (0, 3):
+        s = M.Solver(M.Problem(P.config(1)), schedule=sched)
+        r = s.solve(tol_k=1e-9, tol_src=1e-8, max_iter=2000, check_every=5)
+        assert r["converged"]
+        assert r["k"] == pytest.approx(1.5, abs=1e-5)
+        phi = s.scalar_flux()
+        assert np.ptp(phi) / phi.mean() < 1e-5
 
 
 def test_cfg1_multigroup_k_inf(M, oracle_mod):
     prob = P.config1("7g")
-    s = M.Solver(M.Problem(prob))
-    r = s.solve(tol_k=1e-9, tol_src=1e-7, max_iter=5000)
     m = prob["materials"][0]
     A = np.diag(m["sigma_t"]) - np.array(m["sigma_s"]).T
     kd = max(abs(np.linalg.eigvals(np.linalg.solve(A, np.outer(m["chi"], m["nu_sigma_f"])))))
-    assert r["k"] == pytest.approx(kd, abs=1e-5)
+    for sched in (0, 3):
+        s = M.Solver(M.Problem(prob), schedule=sched)
+        r = s.solve(tol_k=1e-9, tol_src=1e-7, max_iter=5000)
+        assert r["k"] == pytest.approx(kd, abs=1e-5)
 
 
-@pytest.mark.parametrize("schedule", [0, 1, 2])
-def test_fixed_iteration_parity_small_lattice(M, oracle_mod, schedule):
+@pytest.mark.parametrize("schedule,opt", [(0, {}), (1, {}), (2, {}), (3, {}),
+                                          (0, dict(v2_lane_stride=1)), (0, dict(v2_lane_stride=4)),
+                                          (0, dict(v2_lane_stride=8)),
+                                          (3, dict(sc_lanes_per_cell=2)), (3, dict(sc_lanes_per_cell=4)),
+                                          (3, dict(sc_lanes_per_cell=8))])
+def test_fixed_iteration_parity_small_lattice(M, oracle_mod, parity_log, schedule, opt):
+    """Every schedule, forced v2 lane strides 1/4/8 (the benched config runs at 4-8) and
+    forced stack-collective lanes per cell 2/4/8."""
     prob = P.small_lattice(3, 3, 4)
-    s = M.Solver(M.Problem(prob), schedule=schedule)
+    s = M.Solver(M.Problem(prob), schedule=schedule, **opt)
     k, _ = s.iterate(8)
     _check_emitted(s)
     ref = oracle_mod.Oracle(prob).solve(fixed_iters=8)
-    assert k == pytest.approx(ref["k"], abs=1e-5)
-    linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
-    assert linf < 1e-4, (linf, rel)
+    _check(parity_log, f"small_lattice_it8_s{schedule}_{opt}", k, ref["k"], s.scalar_flux(), ref["phi"])
     kh, _ = s.history()
-    np.testing.assert_allclose(kh, ref["k_hist"], atol=1e-5)
+    np.testing.assert_allclose(kh, ref["k_hist"], atol=TOL_K)
 
 
+@pytest.mark.parametrize("schedule", [0, 3])
 @pytest.mark.parametrize("G", [1, 2, 3, 4, 5, 8])
-def test_other_group_counts_parity(M, oracle_mod, G):
+def test_other_group_counts_parity(M, oracle_mod, parity_log, G, schedule):
     """Every group-count instantiation of the sweep (G = 1, 2, 3 -> 4, 4, 5 -> 8 padded,
-    and G = 8 where the source has no pad slot and the material comes from mat[]):
-    fixed-iteration parity against the oracle on a small heterogeneous lattice."""
+    and G = 8 where the source has no pad slot and the material comes from mat[])."""
     prob = P.small_lattice(3, 3, 4, xs=P.xs_synthetic(G))
-    s = M.Solver(M.Problem(prob))
+    s = M.Solver(M.Problem(prob), schedule=schedule)
     k, _ = s.iterate(6)
     _check_emitted(s)
     ref = oracle_mod.Oracle(prob).solve(fixed_iters=6)
-    assert k == pytest.approx(ref["k"], abs=1e-5)
-    linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
-    assert linf < 1e-4, (linf, rel)
+    _check(parity_log, f"small_lattice_G{G}_it6_s{schedule}", k, ref["k"], s.scalar_flux(), ref["phi"])
 
 
 @pytest.mark.parametrize("tile_cells", [4, 9, 37])
-def test_many_chunk_tiles_parity(M, oracle_mod, tile_cells):
+def test_many_chunk_tiles_parity(M, oracle_mod, parity_log, tile_cells):
     """Force tiny shared-memory tally chunks so every work unit is walked in many
     resumable pieces (both directions): results must not depend on the chunking."""
     prob = P.small_lattice(3, 3, 4)
@@ -94,13 +121,11 @@ def test_many_chunk_tiles_parity(M, oracle_mod, tile_cells):
     k, _ = s.iterate(6)
     _check_emitted(s)
     ref = oracle_mod.Oracle(prob).solve(fixed_iters=6)
-    assert k == pytest.approx(ref["k"], abs=1e-5)
-    linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
-    assert linf < 1e-4, (linf, rel)
+    _check(parity_log, f"small_lattice_tiles{tile_cells}", k, ref["k"], s.scalar_flux(), ref["phi"])
 
 
 @pytest.mark.parametrize("budget_mb", [0, 1])
-def test_exp_preload_parity(M, oracle_mod, budget_mb):
+def test_exp_preload_parity(M, oracle_mod, parity_log, budget_mb):
     """§4.2 EXP option: preloaded units replay stored segments in both
     directions (budget 0 = everything that fits 80% of free memory, 1 MiB = hybrid).
     Same physics as OTF (S:348 mode equivalence): k and phi match the oracle and OTF."""
@@ -116,24 +141,70 @@ def test_exp_preload_parity(M, oracle_mod, budget_mb):
     k, _ = s.iterate(3)
     _check_emitted(s)
     ref = oracle_mod.Oracle(prob).solve(fixed_iters=3)
-    assert k == pytest.approx(ref["k"], abs=1e-5)
-    linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
-    assert linf < 1e-4, (linf, rel)
+    _check(parity_log, f"cfg3_reduced_exp{budget_mb}", k, ref["k"], s.scalar_flux(), ref["phi"])
     s0 = M.Solver(pr)
     k0, _ = s0.iterate(3)
     assert k == pytest.approx(k0, abs=1e-6)
 
 
-def test_cfg2_converged_parity(M, oracle_mod):
+@pytest.mark.parametrize("schedule", [0, 3])
+def test_cfg2_converged_parity(M, oracle_mod, parity_log, schedule):
     prob = P.config(2)
-    s = M.Solver(M.Problem(prob))
+    s = M.Solver(M.Problem(prob), schedule=schedule)
     r = s.solve(tol_k=1e-8, tol_src=1e-7, max_iter=5000)
     ref = oracle_mod.Oracle(prob).solve(max_iter=5000, tol_k=1e-10, tol_src=1e-9)
-    assert r["k"] == pytest.approx(ref["k"], abs=1e-5)
-    linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
-    assert linf < 1e-4, (linf, rel)
+    _check(parity_log, f"cfg2_converged_s{schedule}", r["k"], ref["k"], s.scalar_flux(), ref["phi"],
+           iters_gpu=r["iterations"], iters_oracle=ref["iterations"])
     b = s.balance()
     assert b["production"] / r["k"] == pytest.approx(b["absorption"] + b["leakage"], rel=1e-4)
+
+
+@pytest.mark.parametrize("schedule", [
+    pytest.param(0, marks=pytest.mark.xfail(strict=True, reason=(
+        "schedule 0 (round-1 per-track kernel) accumulates the tally in a per-unit u32 fixed "
+        "point scaled by the unit's max psi/source: low-flux FSRs lose digits, per-element "
+        "error 2e-3 at convergence (DESIGN.md §5); the product kernel is schedule 3"))),
+    3])
+def test_cfg3_assembly_converged_parity(M, parity_log, schedule):
+    """C5G7 UO2 assembly geometry (cfg3) with coarser tracking, CONVERGED on both sides at
+    the parity setting (tol_k 1e-7, tol_src 1e-6; §5.1 compares converged k):
+    the oracle's golden took 6113 power iterations (dominance ratio ~0.998).  The GPU runs
+    the same fixed iteration count, so both sit at the same point of the same Jacobi
+    trajectory, and also converges on its own criterion."""
+    g = _golden("cfg3_reduced")
+    prob = P.with_quadrature(P.config(3), num_azim=8, num_polar=4, radial_spacing=0.5, axial_spacing=3.0)
+    s = M.Solver(M.Problem(prob), schedule=schedule)
+    n = int(g["iterations"])
+    k, _ = s.iterate(n)
+    _check(parity_log, f"cfg3_reduced_converged_N{n}_s{schedule}", k, float(g["k"]), s.scalar_flux(), g["phi"])
+    s.reset()
+    r = s.solve(tol_k=float(g["tol_k"]), tol_src=float(g["tol_src"]), max_iter=20000, check_every=1)
+    assert r["converged"]
+    assert abs(r["k"] - float(g["k"])) < TOL_K
+    assert abs(r["iterations"] - n) <= 0.02 * n, (r["iterations"], n)
+
+
+@pytest.mark.parametrize("schedule", [0, 3])
+@pytest.mark.parametrize("case,make", [
+    ("cfg3_it12", lambda: P.config(3)),
+    ("cfg4_it5", lambda: P.config(4)),
+    ("cfg3_fine_it2", lambda: P.with_quadrature(P.config(3), radial_spacing=0.05, axial_spacing=0.1)),
+])
+def test_full_size_fixed_iteration_golden(M, parity_log, case, make, schedule):
+    """BASELINE sizes in the launch configuration bench.py times: k history and sampled
+    FSR fluxes after N power iterations from phi = 1, k = 1, psi = 0 against the fp64
+    oracle (SURVEY §8(c) fixed-N parity: cfg4 N = 5).  cfg3_fine = the assembly at cfg5's
+    tracking (0.05 cm / 0.1 cm: dz = 0.10-0.28 cm, the v2 sweep's lane strides 4 and 8)."""
+    g = _golden(case)
+    s = M.Solver(M.Problem(make()), schedule=schedule)
+    n = int(g["fixed_iters"])
+    k, _ = s.iterate(n)
+    _check_emitted(s)
+    phi = s.scalar_flux().reshape(-1)[g["sample_idx"]]
+    _check(parity_log, f"{case}_s{schedule}", k, float(g["k"]), phi, g["phi_sample"], phimax=float(g["phi_max"]),
+           sampled=int(g["sample_idx"].size))
+    kh, _ = s.history()
+    np.testing.assert_allclose(kh, g["k_hist"], atol=TOL_K)
 
 
 def test_volumes_and_checksums_cfg2(M, oracle_mod):
@@ -141,20 +212,23 @@ def test_volumes_and_checksums_cfg2(M, oracle_mod):
     pr = M.Problem(prob)
     s = M.Solver(pr)
     o = oracle_mod.Oracle(prob)
-    vt, _ = o.volumes()
+    vt, va = o.volumes()
     np.testing.assert_allclose(s.fsr_volumes(), vt, rtol=1e-10)
+    vt_abi, va_abi = s.fsr_volumes(analytic=True)
+    np.testing.assert_allclose(vt_abi, vt, rtol=1e-10)
+    np.testing.assert_allclose(va_abi, va, rtol=1e-12)
     d = s.checksums()
     c = o.checksums()
     assert np.array_equal(d["nseg"], c["nseg"])
     assert np.array_equal(d["hash"], c["hash"])
-    np.testing.assert_allclose(d["suml"], c["suml"], rtol=1e-11)
+    np.testing.assert_allclose(d["suml"], c["suml"], rtol=1e-11, atol=1e-12)
     assert s.timings()["n_segs3d"] == int(c["nseg"].sum())
 
 
-@pytest.mark.parametrize("cfg", [3, 4])
+@pytest.mark.parametrize("cfg", [3, 4, 5])
 def test_checksums_full_size_sampled(M, oracle_mod, cfg):
-    """Full BASELINE sizes: per-track segment counts and FSR hashes on a sample of
-    tracks, bit-exact, in the same solver the bench times; exact total volume."""
+    """Full BASELINE sizes (cfg5 = the benched config): per-track segment counts and FSR
+    hashes of the device OTF walk on a sample of tracks, bit-exact; exact total volume."""
     prob = P.config(cfg)
     pr = M.Problem(prob)
     s = M.Solver(pr)
@@ -167,40 +241,10 @@ def test_checksums_full_size_sampled(M, oracle_mod, cfg):
         c = o.checksums(int(first), 2000)
         assert np.array_equal(d["nseg"], c["nseg"])
         assert np.array_equal(d["hash"], c["hash"])
-        np.testing.assert_allclose(d["suml"], c["suml"], rtol=1e-11)
+        np.testing.assert_allclose(d["suml"], c["suml"], rtol=1e-11, atol=1e-12)
     W = prob["lattice"]["nx"] * prob["lattice"]["pitch_x"]
     Z = prob["axial"]["planes"][-1]
     assert s.fsr_volumes().sum() == pytest.approx(W * W * Z, rel=1e-10)
-
-
-@pytest.mark.parametrize("cfg,iters", [(3, 3), (4, 2)])
-def test_full_size_fixed_iteration_parity(M, oracle_mod, cfg, iters):
-    """BASELINE sizes in the launch configuration bench.py times (schedule 0, default
-    tiles): k and every FSR flux after `iters` power iterations from phi = 1, k = 1,
-    psi = 0 against the fp64 oracle (fixed-N parity for cfg4)."""
-    prob = P.config(cfg)
-    s = M.Solver(M.Problem(prob))
-    k, _ = s.iterate(iters)
-    _check_emitted(s)
-    ref = oracle_mod.Oracle(prob).solve(fixed_iters=iters)
-    assert k == pytest.approx(ref["k"], abs=1e-5)
-    linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
-    assert linf < 1e-4, (linf, rel)
-    kh, _ = s.history()
-    np.testing.assert_allclose(kh, ref["k_hist"], atol=1e-5)
-
-
-def test_cfg3_reduced_fixed_iterations(M, oracle_mod):
-    """C5G7 assembly geometry with coarser tracking (many work units, ragged
-    stacks): 3 fixed iterations against the oracle."""
-    prob = P.with_quadrature(P.config(3), num_azim=8, num_polar=4, radial_spacing=0.5, axial_spacing=3.0)
-    s = M.Solver(M.Problem(prob))
-    k, _ = s.iterate(3)
-    _check_emitted(s)
-    ref = oracle_mod.Oracle(prob).solve(fixed_iters=3)
-    assert k == pytest.approx(ref["k"], abs=1e-5)
-    linf, rel = _flux_err(s.scalar_flux(), ref["phi"])
-    assert linf < 1e-4, (linf, rel)
 
 
 def test_interleaved_solvers_keep_their_constants(M):

@@ -35,6 +35,9 @@ CASES = {
     "cfg3_fine_it2": (lambda: P.with_quadrature(P.config(3), radial_spacing=0.05, axial_spacing=0.1), 2, 60000),
     # BASELINE configs[1] (C5G7 Rodded B), SURVEY §8(c) fixed-N = 5
     "cfg4_it5": (lambda: P.config(4), 5, 60000),
+    # BASELINE configs[4] (the benched config): SURVEY §8(c) fixed-N = 2 (the oracle
+    # re-traces every sweep: ~32 GB of fp64 boundary psi, ~20 min per iteration on 6 cores)
+    "cfg5_it2": (lambda: P.config(5), 2, 60000),
 }
 
 
