@@ -924,7 +924,7 @@ void sc_smem_configure(moc_solver* s) {
   CUDA_OK(cudaFuncGetAttributes(&fa, k_sweep_sc<G, GP, false>));
   const size_t per_cta = (228 * 1024) / kScMinBlocks - 1024 - fa.sharedSizeBytes;
   constexpr int NH = ScH<G>::NH;
-  const size_t stage = (size_t)kScWarps * 32 * 128;  // per-warp cell staging (fast paths)
+  const size_t stage = (size_t)kScWarps * 32 * 64;  // per-warp cell staging (fast path)
   int pcap = s->opts.sc_psi_cap > 0 ? s->opts.sc_psi_cap : (int)((per_cta - stage) / ((size_t)kScWarps * NH * 16));
   pcap = std::max(32, pcap & ~31);
   s->sc_pcap = pcap;

@@ -56,7 +56,6 @@ constexpr int kScThreads = 32 * kScWarps;
 #endif
 constexpr int kScMinBlocks = MOC_SC_CTAS_PER_SM;
 constexpr float kScSliverGuard = 4e-5f;      // fp32 corner length below which fp64 decides
-constexpr float kScLazyMin = 1e-20f;         // lazy map factor below which a set is re-materialised
 
 // debug statistics build (-DMOC_SC_STATS): per-sweep counts of the work decomposition
 #ifdef MOC_SC_STATS
@@ -292,211 +291,6 @@ struct ScCell {
     SC_STAT(4, n);
   }
 
-  // ---- lazy full-crossing sets (one lane per cell).  All full members of a
-  // cell receive the same affine update psi' = E psi + q (1 - E) (Eq. 3 with the shared
-  // Eq. 8 length), so the members of a layer are kept as psi~ with psi = zA psi~ + zB for
-  // the layer's map (zA, zB) and zS = sum psi~: a column's full update is one map update
-  // per cell, its tally (1 - E)(zA zS + n zB - n q) (Eq. 4).  Only corner members (crossing
-  // a plane) touch their own psi; they leave the layer's set and join the next one.
-  __device__ __forceinline__ void lz_sum(int a, int b, int c, float* zS) {  // raw psi: zS = sum
-#pragma unroll
-    for (int g = 0; g < G; ++g) zS[g] = 0.f;
-    if (a >= b) return;
-    visit<10, 11>(
-        a, b, 0, 0, c,
-        [&](int m0, int m1) {
-          float v0[4 * NH], v1[4 * NH];
-          load(m0, v0);
-          load(m1, v1);
-#pragma unroll
-          for (int g = 0; g < G; ++g) zS[g] += v0[g] + v1[g];
-        },
-        [&](int m) {
-          float v[4 * NH];
-          load(m, v);
-#pragma unroll
-          for (int g = 0; g < G; ++g) zS[g] += v[g];
-        });
-  }
-  // psi~ -> psi = A psi~ + Bv in place (optionally zS = sum of the new psi)
-  template <bool SUM>
-  __device__ __forceinline__ void lz_materialize(int a, int b, int c, const float* A, const float* Bv, float* zS) {
-    if constexpr (SUM) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) zS[g] = 0.f;
-    }
-    if (a >= b) return;
-    visit<12, 13>(
-        a, b, 0, 0, c,
-        [&](int m0, int m1) {
-          float v0[4 * NH], v1[4 * NH];
-          load(m0, v0);
-          load(m1, v1);
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            v0[g] = fmaf(A[g], v0[g], Bv[g]);
-            v1[g] = fmaf(A[g], v1[g], Bv[g]);
-            if constexpr (SUM) zS[g] += v0[g] + v1[g];
-          }
-          store(m0, v0);
-          store(m1, v1);
-        },
-        [&](int m) {
-          float v[4 * NH];
-          load(m, v);
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            v[g] = fmaf(A[g], v[g], Bv[g]);
-            if constexpr (SUM) zS[g] += v[g];
-          }
-          store(m, v);
-        });
-  }
-  // corner members of a lazy layer: materialise (old map, leave the set: zS -= psi~),
-  // pieces 1 and 2 as corner2, then (join) enter the layer above's set (its published
-  // post-column map (A2, B2): psi~ = (psi - B2) / A2, Sj += psi~); above the domain top or
-  // into a layer outside the band's window psi stays raw
-  __device__ __forceinline__ void lz_corner2(int a, int b, int c, float d1a, float d2a, float dzf, float ti, bool nxt,
-                                             bool join, int skip1, int skip2, const float4* st2, uint32_t j2, float* T2,
-                                             const float* zA, const float* zB, float* zS, float* Sj) {
-    if (a >= b) return;
-    float q2[8], sg2[8], b2[8], i2[8];
-    {
-      const float4 x0 = st2[0], x1 = st2[32], y0 = st2[64], y1 = st2[96];
-      const float4 u0 = st2[128], u1 = st2[160], w0 = st2[192], w1 = st2[224];
-      q2[0] = x0.x; q2[1] = x0.y; q2[2] = x0.z; q2[3] = x0.w;
-      q2[4] = x1.x; q2[5] = x1.y; q2[6] = x1.z; q2[7] = x1.w;
-      sg2[0] = y0.x; sg2[1] = y0.y; sg2[2] = y0.z; sg2[3] = y0.w;
-      sg2[4] = y1.x; sg2[5] = y1.y; sg2[6] = y1.z; sg2[7] = y1.w;
-      i2[0] = u0.x; i2[1] = u0.y; i2[2] = u0.z; i2[3] = u0.w;
-      i2[4] = u1.x; i2[5] = u1.y; i2[6] = u1.z; i2[7] = u1.w;
-      b2[0] = w0.x; b2[1] = w0.y; b2[2] = w0.z; b2[3] = w0.w;
-      b2[4] = w1.x; b2[5] = w1.y; b2[6] = w1.z; b2[7] = w1.w;
-#pragma unroll
-      for (int g = 0; g < G; ++g) asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(i2[g]) : "f"(i2[g]));
-    }
-    const float t2 = nxt ? ti : 0.f;
-    auto one = [&](int m, float* v) {
-      const float L1 = m == skip1 ? 0.f : fmaf((float)(b - 1 - m), dzf, d1a) * ti;
-      const float L2 = m == skip2 ? 0.f : fmaf((float)(m - a), dzf, d2a) * t2;
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        zS[g] -= v[g];
-        float x = fmaf(zA[g], v[g], zB[g]);
-        const float E1 = ex2_approx(-sg[g] * L1);
-        const float e1 = x - q[g];
-        const float l1 = fmaf(-e1, E1, e1);
-        x -= l1;
-        T[g] += l1;
-        const float E2 = ex2_approx(-sg2[g] * L2);
-        const float e2 = x - q2[g];
-        const float l2 = fmaf(-e2, E2, e2);
-        x -= l2;
-        T2[g] += l2;
-        if (join) {
-          x = (x - b2[g]) * i2[g];
-          Sj[g] += x;
-        }
-        v[g] = x;
-      }
-    };
-    auto emit = [&](int m) {
-      if constexpr (HASH) {
-        if (m != skip1) emit_hash(m);
-        if (nxt && m != skip2) {
-          hh[m] = sc_fnv(hh[m], j2);
-          hc[m] += 1;
-        }
-      }
-    };
-    const int n = visit<7, 9>(
-        a, b, 0, 0, c,
-        [&](int m0, int m1) {
-          float v0[4 * NH], v1[4 * NH];
-          load(m0, v0);
-          load(m1, v1);
-          one(m0, v0);
-          one(m1, v1);
-          store(m0, v0);
-          store(m1, v1);
-          emit(m0);
-          emit(m1);
-        },
-        [&](int m) {
-          float v[4 * NH];
-          load(m, v);
-          one(m, v);
-          store(m, v);
-          emit(m);
-        });
-    nem += nxt ? 2 * n : n;
-    if (skip1 >= 0) --nem;
-    if (nxt && skip2 >= 0) --nem;
-    SC_STAT(4, 2 * n);
-  }
-  // members entering cell 0 through the domain bottom (raw psi): one bottom -> right piece
-  // (length d(m) = d0 + (m - a) dz), then they join layer 0's set (map (A0, B0) published by
-  // its lane: psi~ = (psi - B0) / A0, Sj += psi~); tally share -> Tb
-  __device__ __forceinline__ void lz_bottom(int a, int b, int c, float d0, float dzf, float ti, const float4* st0,
-                                            float* Tb, float* Sj) {
-    if (a >= b) return;
-    float q0[8], sg0[8], b0[8], i0[8];
-    {
-      const float4 x0 = st0[0], x1 = st0[32], y0 = st0[64], y1 = st0[96];
-      const float4 u0 = st0[128], u1 = st0[160], w0 = st0[192], w1 = st0[224];
-      q0[0] = x0.x; q0[1] = x0.y; q0[2] = x0.z; q0[3] = x0.w;
-      q0[4] = x1.x; q0[5] = x1.y; q0[6] = x1.z; q0[7] = x1.w;
-      sg0[0] = y0.x; sg0[1] = y0.y; sg0[2] = y0.z; sg0[3] = y0.w;
-      sg0[4] = y1.x; sg0[5] = y1.y; sg0[6] = y1.z; sg0[7] = y1.w;
-      i0[0] = u0.x; i0[1] = u0.y; i0[2] = u0.z; i0[3] = u0.w;
-      i0[4] = u1.x; i0[5] = u1.y; i0[6] = u1.z; i0[7] = u1.w;
-      b0[0] = w0.x; b0[1] = w0.y; b0[2] = w0.z; b0[3] = w0.w;
-      b0[4] = w1.x; b0[5] = w1.y; b0[6] = w1.z; b0[7] = w1.w;
-#pragma unroll
-      for (int g = 0; g < G; ++g) asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(i0[g]) : "f"(i0[g]));
-    }
-    const int n = visit<7, 9>(
-        a, b, 0, 0, c,
-        [&](int m0, int m1) {
-          const float L0 = fmaf((float)(m0 - a), dzf, d0) * ti, L1 = fmaf((float)(m1 - a), dzf, d0) * ti;
-          float v0[4 * NH], v1[4 * NH];
-          load(m0, v0);
-          load(m1, v1);
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const float E0 = ex2_approx(-sg0[g] * L0), E1 = ex2_approx(-sg0[g] * L1);
-            const float e0 = v0[g] - q0[g], e1 = v1[g] - q0[g];
-            const float l0 = fmaf(-e0, E0, e0), l1 = fmaf(-e1, E1, e1);
-            Tb[g] += l0 + l1;
-            v0[g] = (v0[g] - l0 - b0[g]) * i0[g];
-            v1[g] = (v1[g] - l1 - b0[g]) * i0[g];
-            Sj[g] += v0[g] + v1[g];
-          }
-          store(m0, v0);
-          store(m1, v1);
-          emit_hash(m0);
-          emit_hash(m1);
-        },
-        [&](int m) {
-          const float L = fmaf((float)(m - a), dzf, d0) * ti;
-          float v[4 * NH];
-          load(m, v);
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const float E = ex2_approx(-sg0[g] * L);
-            const float e = v[g] - q0[g];
-            const float l = fmaf(-e, E, e);
-            Tb[g] += l;
-            v[g] = (v[g] - l - b0[g]) * i0[g];
-            Sj[g] += v[g];
-          }
-          store(m, v);
-          emit_hash(m);
-        });
-    nem += n;
-    SC_STAT(4, n);
-  }
-
   // fast-path corner class (rho < h_min): members entering cell l through its left face
   // and leaving through its top plane P_u into cell l + 1, whose right face they reach
   // before the next plane.  Piece 1 (cell l): d1(m) = P_u - z_m = d1a + (b - 1 - m) dz;
@@ -592,8 +386,8 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
   const int pcap = a.pcap;
   float4* const psl = dsm_sc + (size_t)warp * NH * pcap;
   // per-warp cell staging (fast path), SoA [4][32 lanes] float4: q[0..7], sigma_t log2(e)[0..7]
-  float4* const stg = dsm_sc + (size_t)kScWarps * NH * pcap + (size_t)warp * 32 * 8;
-  float4* const hbase = dsm_sc + (size_t)kScWarps * NH * pcap + (size_t)kScWarps * 32 * 8;
+  float4* const stg = dsm_sc + (size_t)kScWarps * NH * pcap + (size_t)warp * 32 * 4;
+  float4* const hbase = dsm_sc + (size_t)kScWarps * NH * pcap + (size_t)kScWarps * 32 * 4;
   uint64_t* const hh = HASH ? reinterpret_cast<uint64_t*>(hbase) + (size_t)warp * pcap : nullptr;
   int* const hc =
       HASH ? reinterpret_cast<int*>(reinterpret_cast<uint64_t*>(hbase) + (size_t)kScWarps * pcap) + (size_t)warp * pcap
@@ -656,15 +450,6 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
       cell.hh = hh;
       cell.hc = hc;
       cell.nem = 0;
-      // lazy layer sets (units with one lane per cell): lane -> layer zl by the ring map
-      // l = lane (mod 32); zinit: every member still holds raw psi (unit start, or after a
-      // general-path column); [zlo, zhi) = the lane's layer members at the next column start
-      const bool lazy = lgR == 0;
-      bool zinit = true;
-      int zl = -1, zlo = 0, zhi = 0;
-      float zA[G], zB[G], zS[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) zA[g] = 1.f, zB[g] = 0.f, zS[g] = 0.f;
 #pragma unroll 1
       for (int kk = 0; kk < nk; ++kk) {
         const int k = ms ? nk - 1 - kk : kk;
@@ -684,19 +469,11 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
           if (lane == 0) atomicAdd(a.err, 1);
           Lh = L_lo + C - 1;
         }
-        const int l = lazy ? L_lo + ((lane - L_lo) & 31) : L_lo + ci;
+        const int l = L_lo + ci;
         const bool act = l <= Lh;
         if (lane == 0) SC_STAT(1, 1), SC_STAT(2, Lh - L_lo + 1);
         auto Uf = [&](double x) {
           const int v = __double2int_ru((x - base) * invD);
-          return min(max(v, 0), B);
-        };
-        // the band's base at the column's right face = the next column's base, bit for bit
-        // (lazy path: membership at the end of a column is decided exactly as the next
-        // column decides it at its start)
-        const double base_next = zc0 + (ms ? Lt - s_a : s_b) * c;
-        auto Ufn = [&](double x) {
-          const int v = __double2int_ru((x - base_next) * invD);
           return min(max(v, 0), B);
         };
         const uint32_t region = d.seg_region[sb + k];
@@ -729,150 +506,13 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
           for (int g = 0; g < 8; ++g) cell.q[g] = g < G ? qv[g] : 0.f;
           Pl = P[l];
           Pu = P[l + 1];
-          if (!lazy || !(rho < a.h_fast)) {
-            uPlR = Uf(Pl - rho);
-            uPuR = Uf(Pu - rho);
-          }
+          uPlR = Uf(Pl - rho);
+          uPuR = Uf(Pu - rho);
           uPl = Uf(Pl);
           uPu = Uf(Pu);
         }
         const bool fast = rho < a.h_fast;  // every member crosses at most one plane here
-        const bool spare = lgR == 0 && Lh - L_lo + 1 < 32;  // lane 31 has no cell this column
-        if (lazy && fast) {
-          // ---------------- lazy one-crossing column (one lane per cell)
-          if (act && (zinit || zl != l)) {
-            // (re)start this layer's set from raw psi: unit start / after a general column /
-            // a layer entering the window (its members, if any, hold raw psi)
-            zl = l;
-#pragma unroll
-            for (int g = 0; g < G; ++g) zA[g] = 1.f, zB[g] = 0.f;
-            cell.lz_sum(uPl, uPu, lane, zS);
-          }
-          zinit = false;
-          float E[G];
-          bool ren = false;
-          float pa[8], pb[8];
-#pragma unroll
-          for (int g = 0; g < 8; ++g) pa[g] = 1.f, pb[g] = 0.f;
-          if (act) {
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-              E[g] = ex2_approx(-cell.sg[g] * Lf);
-              pa[g] = zA[g] * E[g];
-              pb[g] = fmaf(zB[g], E[g], cell.q[g] * (1.f - E[g]));
-              ren |= pa[g] < kScLazyMin;
-            }
-          } else {
-#pragma unroll
-            for (int g = 0; g < 8; ++g) cell.q[g] = cell.sg[g] = 0.f;
-          }
-          // staging [8][32] float4: q, sigma_t log2(e), published post-column map (identity
-          // when the set is re-materialised this column)
-          stg[lane] = make_float4(cell.q[0], cell.q[1], cell.q[2], cell.q[3]);
-          stg[32 + lane] = make_float4(cell.q[4], cell.q[5], cell.q[6], cell.q[7]);
-          stg[64 + lane] = make_float4(cell.sg[0], cell.sg[1], cell.sg[2], cell.sg[3]);
-          stg[96 + lane] = make_float4(cell.sg[4], cell.sg[5], cell.sg[6], cell.sg[7]);
-          stg[128 + lane] = ren ? make_float4(1.f, 1.f, 1.f, 1.f) : make_float4(pa[0], pa[1], pa[2], pa[3]);
-          stg[160 + lane] = ren ? make_float4(1.f, 1.f, 1.f, 1.f) : make_float4(pa[4], pa[5], pa[6], pa[7]);
-          stg[192 + lane] = ren ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(pb[0], pb[1], pb[2], pb[3]);
-          stg[224 + lane] = ren ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(pb[4], pb[5], pb[6], pb[7]);
-          __syncwarp();
-          float Sj[G];
-#pragma unroll
-          for (int g = 0; g < G; ++g) Sj[g] = 0.f;
-          if (act) {
-            const int UuN = Ufn(Pu);
-            const int uF = max(uPl, min(uPu, UuN));
-            // corner members: left -> top in l, bottom -> right in l + 1; they join l + 1's
-            // set when l + 1 is in the window (else they keep raw psi for its first column)
-            const int a0 = max(uPl, UuN), b0 = uPu;
-            if (a0 < b0) {
-              const bool nxt = l + 1 < NL;
-              const bool join = nxt && l + 1 <= Lh;
-              const int lp2 = mz ? lp - 1 : lp + 1;
-              const double d1 = Pu - (base + (double)(b0 - 1) * dz);    // shortest piece 1: member b0 - 1
-              const double d2 = base_next + (double)a0 * dz - Pu;       // shortest piece 2: member a0
-              int skip1 = -1, skip2 = -1;
-              if ((float)d1 * ti < kScSliverGuard) {
-                const int mphys = mz ? B - 1 - (b0 - 1) : b0 - 1;
-                const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
-                if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) skip1 = b0 - 1;
-              }
-              if (nxt && (float)d2 * ti < kScSliverGuard) {
-                const int mphys = mz ? B - 1 - a0 : a0;
-                const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
-                if (sc_walk_len(d, shP[0], sb, k, lp2, z0, tn, isn, Lt, up) < kEpsL) skip2 = a0;
-              }
-              cell.lz_corner2(a0, b0, lane, (float)d1, (float)d2, dzf, ti, nxt, join, skip1, skip2,
-                              stg + ((lane + 1) & 31), region * (uint32_t)NL + (uint32_t)lp2, T2, zA, zB, zS, Sj);
-            }
-            // the full set (Eq. 8 pieces): one map update and the aggregated tally
-            const int n = uF - uPl;
-            if (n > 0) {
-              const float fn = (float)n;
-#pragma unroll
-              for (int g = 0; g < G; ++g)
-                cell.T[g] = fmaf(1.f - E[g], fmaf(zA[g], zS[g], fn * zB[g]) - fn * cell.q[g], cell.T[g]);
-              cell.nem += n;
-              SC_STAT(3, n);
-              if constexpr (HASH) {
-                for (int m = uPl; m < uF; ++m) cell.emit_hash(m);
-              }
-            }
-            if (ren) {
-              cell.template lz_materialize<true>(uPl, uF, lane, pa, pb, zS);
-#pragma unroll
-              for (int g = 0; g < G; ++g) zA[g] = 1.f, zB[g] = 0.f;
-            } else {
-#pragma unroll
-              for (int g = 0; g < G; ++g) zA[g] = pa[g], zB[g] = pb[g];
-            }
-            // members entering through the domain bottom, when no spare lane takes them
-            if (l == 0 && !spare) {
-              const int U0N = Ufn(0.0);
-              int a1 = U0N;
-              if (a1 < uPl) {
-                const double dbot = base_next + (double)a1 * dz;
-                if ((float)dbot * ti < kScSliverGuard) {
-                  const int mphys = mz ? B - 1 - a1 : a1;
-                  const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
-                  if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) ++a1;
-                }
-                cell.lz_bottom(a1, uPl, lane, (float)(base_next + (double)a1 * dz), dzf, ti, stg + lane, cell.T, zS);
-              }
-            }
-            zlo = Ufn(Pl);  // the layer's members at the next column's start
-            zhi = UuN;
-          } else {
-            zlo = zhi = 0;
-          }
-          if (spare && lane == 31 && L_lo == 0) {
-            // lane 31 acts as layer -1: members entering cell 0 through the domain bottom
-            const int lp0 = mz ? NL - 1 : 0;
-            int a1 = Ufn(0.0);
-            const int b1 = Uf(0.0);
-            if (a1 < b1) {
-              const double dbot = base_next + (double)a1 * dz;
-              if ((float)dbot * ti < kScSliverGuard) {
-                const int mphys = mz ? B - 1 - a1 : a1;
-                const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
-                if (sc_walk_len(d, shP[0], sb, k, lp0, z0, tn, isn, Lt, up) < kEpsL) ++a1;
-              }
-              cell.j = region * (uint32_t)NL + (uint32_t)lp0;
-              cell.lz_bottom(a1, b1, lane, (float)(base_next + (double)a1 * dz), dzf, ti, stg, T2, Sj);
-            }
-          }
-          // cell l + 1's tally shares and joining members' psi~ -> the lane of layer l + 1
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const float x = __shfl_sync(0xffffffffu, T2[g], (lane - 1) & 31);
-            const float y = __shfl_sync(0xffffffffu, Sj[g], (lane - 1) & 31);
-            if (act && (l > L_lo || (spare && l == 0))) {
-              cell.T[g] += x;
-              zS[g] += y;
-            }
-          }
-        } else if (fast) {
+        if (fast) {
           if (!act) {  // finite staging for lanes without a cell (read only with zero lengths)
 #pragma unroll
             for (int g = 0; g < 8; ++g) cell.q[g] = cell.sg[g] = 0.f;
@@ -906,9 +546,8 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
               cell.corner2(a0, b0, r, lgR, ci, (float)d1, (float)d2, dzf, ti, nxt, skip1, skip2, stg + ((lane + R) & 31),
                            region * (uint32_t)NL + (uint32_t)lp2, T2);
             }
-            // members entering through the domain bottom (canonical z' = 0) in this column:
-            // on the spare lane below (next block) when there is one, else here
-            if (l == 0 && !spare && uPlR < uPl) {
+            // members entering through the domain bottom (canonical z' = 0) in this column
+            if (l == 0 && uPlR < uPl) {
               int a1 = uPlR;
               const double dbot = base + (double)a1 * dz + rho - Pl;
               if ((float)dbot * ti < kScSliverGuard) {
@@ -920,46 +559,13 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
                 cell.corner(a1, uPl, r, lgR, ci, a1, (float)(base + (double)a1 * dz + rho - Pl), dzf, ti);
             }
           }
-          if (spare && lane == 31 && L_lo == 0) {
-            // lane 31 has no cell: it acts as layer -1 and sweeps the members entering
-            // cell 0 through the domain bottom (one bottom -> right piece each; cell 0's
-            // source from the staging), its tally share going to lane 0 like a corner's
-            const int lp0 = mz ? NL - 1 : 0;
-            int a1 = Uf(-rho);
-            const int b1 = Uf(0.0);
-            if (a1 < b1) {
-              const double dbot = base + (double)a1 * dz + rho;
-              if ((float)dbot * ti < kScSliverGuard) {
-                const int mphys = mz ? B - 1 - a1 : a1;
-                const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
-                if (sc_walk_len(d, shP[0], sb, k, lp0, z0, tn, isn, Lt, up) < kEpsL) ++a1;
-              }
-              if (a1 < b1) {
-                const float4 x0 = stg[0], x1 = stg[32], y0 = stg[64], y1 = stg[96];  // lane 0 = cell 0
-                cell.q[0] = x0.x; cell.q[1] = x0.y; cell.q[2] = x0.z; cell.q[3] = x0.w;
-                cell.q[4] = x1.x; cell.q[5] = x1.y; cell.q[6] = x1.z; cell.q[7] = x1.w;
-                cell.sg[0] = y0.x; cell.sg[1] = y0.y; cell.sg[2] = y0.z; cell.sg[3] = y0.w;
-                cell.sg[4] = y1.x; cell.sg[5] = y1.y; cell.sg[6] = y1.z; cell.sg[7] = y1.w;
-                cell.j = region * (uint32_t)NL + (uint32_t)lp0;
-                cell.corner(a1, b1, 0, 0, 31, a1, (float)(base + (double)a1 * dz + rho), dzf, ti);
-#pragma unroll
-                for (int g = 0; g < G; ++g) T2[g] = cell.T[g], cell.T[g] = 0.f;
-              }
-            }
-          }
-          // cell l + 1's shares of the corner pieces -> the lanes of cell l + 1 (with a spare
-          // lane 31, lane 0 receives its bottom entries)
+          // cell l + 1's shares of the corner pieces -> the lanes of cell l + 1
 #pragma unroll
           for (int g = 0; g < G; ++g) {
-            const float x = __shfl_sync(0xffffffffu, T2[g], (lane - R) & 31);
-            if (act && (ci > 0 || spare)) cell.T[g] += x;
+            const float x = __shfl_up_sync(0xffffffffu, T2[g], R);
+            if (ci > 0) cell.T[g] += x;
           }
         } else {
-          if (lazy && !zinit) {  // the general path reads raw psi: materialise the layer sets
-            if (act) cell.template lz_materialize<false>(uPl, uPu, lane, zA, zB, nullptr);
-            __syncwarp();
-          }
-          if (lazy) zinit = true;
           int uprev = uPl;
           if (act) {
             // sub-phase 0: members entering through the left face in layer l
@@ -1030,10 +636,6 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
             }
           }
         }
-        __syncwarp();
-      }
-      if (lazy && !zinit) {
-        cell.template lz_materialize<false>(zlo, zhi, lane, zA, zB, nullptr);
         __syncwarp();
       }
       nemit += cell.nem;

@@ -17,8 +17,8 @@ import paper_2503_17743_b200 as M  # noqa: E402
 import problems as P  # noqa: E402
 
 NAMES = ["unit_dirs", "columns", "active_cells", "full_pieces", "corner_pieces", "q_trips", "full_warp_trips",
-         "corner_warp_trips", "full_warp_calls", "corner_warp_calls", "sum_warp_trips", "sum_warp_calls",
-         "mat_warp_trips", "mat_warp_calls", "renorm_warp_trips", "renorm_warp_calls"]
+         "corner_warp_trips", "full_warp_calls", "corner_warp_calls", "mat_warp_trips", "mat_warp_calls",
+         "join_warp_trips", "join_warp_calls", "renorm_warp_trips", "renorm_warp_calls"]
 kw = dict(a.split("=") for a in sys.argv[1:] if "=" in a)
 for cfg in [int(x) for x in sys.argv[1:] if "=" not in x] or [4]:
     L = M.lib()
