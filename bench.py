@@ -212,6 +212,8 @@ def run_ours(args):
     dev = local % max(1, ndev)  # gloo testing: several ranks may share one GPU
     torch.cuda.set_device(dev)
     prob = P.config(args.config)
+    if args.xs:  # real NEA C5G7 tables from a user file (k context only; not the benched data)
+        prob = P.with_xs(prob, P.load_xs_table(args.xs))
     t0 = time.time()
     pr = M.Problem(prob)
     t_lay = time.time() - t0
@@ -341,7 +343,8 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic (seeded C5G7-shaped 7G XS, problems/; deterministic laydown)",
+        "dtype": "f32", "data": ("synthetic (seeded C5G7-shaped 7G XS, problems/; deterministic laydown)" if not args.xs
+                                 else f"C5G7 geometry with user cross sections {os.path.basename(args.xs)}"),
         "config": {"workload": WORKLOADS.get(args.config, f"cfg{args.config}"), "fsr": st["n_fsr"],
                    "tracks3d": st["n_tracks3d"], "segments3d": tm["n_segs3d"], "groups": G,
                    "integrations_per_step": nint, "parallelism": f"tracks partitioned over {world} GPU(s)",
@@ -387,6 +390,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true", help="skip the closed-form k-eff error legs")
     ap.add_argument("--exp", action="store_true", help="EXP/OTF hybrid of §4.2 instead of pure OTF")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
+    ap.add_argument("--xs", default=None, help="C5G7 cross-section table (problems.load_xs_table JSON)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -559,9 +559,7 @@ struct moc_solver {
   uint32_t* d_cost = nullptr;
   uint8_t* d_mat = nullptr;
   float *d_qt = nullptr, *d_phi = nullptr, *d_fold = nullptr, *d_fnew = nullptr;
-  cudaTextureObject_t qtex = 0;  // d_qt as float4 texture (GP = 8; the MOC_V2_QTEX gather)
-  int4 *d_kf = nullptr, *d_kb = nullptr;  // per 2D segment {s_end | s_start, region * NL, 0}
-  cudaTextureObject_t ktf = 0, ktb = 0;   // textures over d_kf / d_kb (MOC_V2_KTEX)
+  cudaTextureObject_t qtex = 0;  // d_qt as float4 texture (GP = 8: the sweeps' source gather)
   double* d_phi64 = nullptr;  // [J][G] staging for moc_get_scalar_flux (allocated on first use)
   double *d_tally = nullptr, *d_vol = nullptr;
   float* d_psi[2] = {nullptr, nullptr};
@@ -584,9 +582,8 @@ struct moc_solver {
   float *d_rmax = nullptr, *d_qmax_t = nullptr, *d_tally32 = nullptr;
   int* d_err = nullptr;
   int cap_cells = 0;  // v2 tile capacity in cells (sweep_v2.cuh layout)
-  int interleave = 1; // v2 sibling units interleaved per member range (Unit::step)
   int tile_off = 0;   // v2 tile byte offset (above the largest unit's tables)
-  int lane_lg = -1;  // forced log2 v2 lane stride (MOC_V2_LANE_STRIDE), -1 = per unit
+  int lane_lg = -1;  // forced log2 v2 lane stride (opts.v2_lane_stride), -1 = per unit
   double h_lane = 0;     // thinnest axial layer / 3 (sweep_v2.cuh lane_lg_of)
   size_t v2_smem = 0;
   uint32_t* d_unit_maxq = nullptr;  // longest track (merged segments) per unit
@@ -711,8 +708,6 @@ void run_sweep(moc_solver* s) {
     a.mat = s->d_mat;
     a.qt = s->d_qt;
     a.qtex = s->qtex;
-    a.ktf = s->ktf;
-    a.ktb = s->ktb;
     a.qmax_t = s->d_qmax_t;
     a.psi_in = s->d_psi[in];
     a.psi_out = s->d_psi[out];
@@ -720,7 +715,6 @@ void run_sweep(moc_solver* s) {
     a.sc = s->d_sc;
     a.tile_off = s->tile_off;
     a.cap_cells = s->cap_cells;
-    a.stage_off = s->tile_off + s->cap_cells * tile_cell_bytes(s->G, s->GP);  // staged sources follow the tile
     a.lane_lg = s->lane_lg;
     a.h_lane = s->h_lane;
     a.err = s->d_err;
@@ -1062,11 +1056,9 @@ void destroy(moc_solver* s) {
                   s->d_link, s->d_work, s->d_cost, s->d_mat, s->d_qt, s->d_phi, s->d_fold, s->d_fnew, s->d_tally,
                   s->d_vol, s->d_psi[0], s->d_psi[1], s->d_sc, s->d_part_a, s->d_part_b, s->d_part_c, s->d_hist,
                   s->d_units, s->d_counter, s->d_rmax, s->d_qmax_t, s->d_tally32, s->d_err,
-                  s->d_unit_maxq, s->d_unit_exp, s->d_store, s->d_phi64, s->d_kf, s->d_kb, s->d_sc_units,
+                  s->d_unit_maxq, s->d_unit_exp, s->d_store, s->d_phi64, s->d_sc_units,
                   s->d_send_slots, s->d_recv_slots, s->d_halo_send, s->d_halo_recv};
   if (s->qtex) cudaDestroyTextureObject(s->qtex);
-  if (s->ktf) cudaDestroyTextureObject(s->ktf);
-  if (s->ktb) cudaDestroyTextureObject(s->ktb);
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : s->ev)
@@ -1201,39 +1193,6 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     s->d_st_first = dmalloc<uint32_t>(s->S + 1, B);
     upload(L.seg_send.data(), s->d_seg_send, 8 * s->N2, st);
     upload(L.seg_region.data(), s->d_seg_region, 4 * s->N2, st);
-    {
-      // radial-step records for the sweep's texture path: forward {s_end, region * NL},
-      // backward {s_start, region * NL} per global 2D segment
-      std::vector<int4> kf((size_t)s->N2), kb((size_t)s->N2);
-      auto pack = [&](double v, int kx) {
-        int64_t b;
-        std::memcpy(&b, &v, 8);
-        return make_int4((int)(uint32_t)(b & 0xffffffffu), (int)(uint32_t)((uint64_t)b >> 32), kx, 0);
-      };
-      for (int64_t t = 0; t < s->T2; ++t)
-        for (int64_t i = L.t_seg[t]; i < L.t_seg[t + 1]; ++i) {
-          const int kx = (int)L.seg_region[i] * g.NL;
-          kf[i] = pack(L.seg_send[i], kx);
-          kb[i] = pack(i == L.t_seg[t] ? 0.0 : L.seg_send[i - 1], kx);
-        }
-      s->d_kf = dmalloc<int4>(s->N2, B);
-      s->d_kb = dmalloc<int4>(s->N2, B);
-      CUDA_OK(cudaMemcpyAsync(s->d_kf, kf.data(), sizeof(int4) * s->N2, cudaMemcpyHostToDevice, st));
-      CUDA_OK(cudaMemcpyAsync(s->d_kb, kb.data(), sizeof(int4) * s->N2, cudaMemcpyHostToDevice, st));
-      CUDA_OK(cudaStreamSynchronize(st));  // the host vectors go out of scope
-      if (s->N2 < (int64_t(1) << 27)) {
-        for (int w = 0; w < 2; ++w) {
-          cudaResourceDesc rd{};
-          rd.resType = cudaResourceTypeLinear;
-          rd.res.linear.devPtr = w ? (void*)s->d_kb : (void*)s->d_kf;
-          rd.res.linear.desc = cudaCreateChannelDesc<int4>();
-          rd.res.linear.sizeInBytes = sizeof(int4) * (size_t)s->N2;
-          cudaTextureDesc td{};
-          td.readMode = cudaReadModeElementType;
-          CUDA_OK(cudaCreateTextureObject(w ? &s->ktb : &s->ktf, &rd, &td, nullptr));
-        }
-      }
-    }
     upload(g.planes.data(), s->d_planes, 8 * (g.NL + 1), st);
     if (g.NL + 1 <= 256) {
       CUDA_OK(cudaMallocHost(&s->h_planes, sizeof(double) * (g.NL + 1)));
@@ -1404,14 +1363,8 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       for (int64_t q = 0; q < s->S; ++q) {
         if (!owner.empty() && owner[q] != s->comm.rank) continue;
         const int64_t cnt = L.st_cnt[q];
-        // R sibling units interleave over each range of R * kV2Threads members (lanes of a
-        // warp then sit R times further apart in z: fewer same-cell shared atomics)
-        const int64_t R = s->interleave;
-        for (int64_t b0 = 0; b0 < cnt; b0 += R * kV2Threads) {
-          const int64_t blk = std::min<int64_t>(R * kV2Threads, cnt - b0);
-          for (int64_t r = 0; r < R && r < blk; ++r)
-            units.push_back(Unit{(uint32_t)q, (uint32_t)(b0 + r), (uint32_t)((blk - r + R - 1) / R), (uint32_t)R});
-        }
+        for (int64_t b0 = 0; b0 < cnt; b0 += kV2Threads)
+          units.push_back(Unit{(uint32_t)q, (uint32_t)b0, (uint32_t)std::min<int64_t>(kV2Threads, cnt - b0), 1u});
       }
       s->n_units = (uint32_t)units.size();
       s->d_units = dmalloc<Unit>(units.size(), B);

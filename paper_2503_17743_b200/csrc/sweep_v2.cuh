@@ -46,33 +46,9 @@ constexpr uint32_t kMagicBits = 0x4B400000u;  // bits of 1.5 * 2^23
 constexpr float kMagic = 12582912.0f;         // 1.5 * 2^23
 constexpr float kFixOne = 2097152.0f;         // 2^21: max |term| in fixed point
 constexpr uint64_t kNoExp = ~0ull;
-#ifndef MOC_V2_Q128
-#define MOC_V2_Q128 0
-#endif
-// MOC_V2_NOCOUNT: tile words receive bits(dpsi' + 1.5 * 2^23) - 0x4B400000 (an IADD per
-// group) instead of the raw bits plus a per-cell count atomic removing the offset at the flush
-#ifndef MOC_V2_NOCOUNT
-#define MOC_V2_NOCOUNT 1
-#endif
-#ifndef MOC_V2_F2I
-#define MOC_V2_F2I 0
-#endif
-#ifndef MOC_V2_KTEX
-#define MOC_V2_KTEX 0
-#endif
-#ifndef MOC_V2_QTEX
-#define MOC_V2_QTEX 1
-#endif
-#ifndef MOC_V2_SIG_CONST
-#define MOC_V2_SIG_CONST 1
-#endif
-#ifndef MOC_V2_PLANES_CONST
-#define MOC_V2_PLANES_CONST 0
-#endif
+// tile words receive bits(dpsi' + 1.5 * 2^23) - 0x4B400000 (offset-free fixed-point codes:
+// an IADD per group instead of a per-cell count atomic removing the offset at the flush)
 static_assert(kMaxPlanes == sizeof(c_planes) / sizeof(double), "c_planes sized for kMaxPlanes");
-#ifndef MOC_V2_PSI_SCALAR
-#define MOC_V2_PSI_SCALAR 0  // 1: per-group 32-bit boundary-psi loads / stores (A/B)
-#endif            // unit not preloaded (on-the-fly)
 // epsilon_L in the constant bank: DSETP reads it as an operand, where the immediate form
 // would cost two uniform moves per raw piece (same value as otf.h kEpsL)
 __constant__ double c_epsL = kEpsL;
@@ -100,34 +76,15 @@ struct __align__(16) KSeg {
 // in different cells on different banks).  The tile never moves and stays zero between
 // flushes.
 __host__ __device__ constexpr int unit_table_bytes(int nk) { return 32 * nk + ((8 * (nk + 1) + 15) & ~15); }
-#ifndef MOC_V2_TILE_COPIES
-#define MOC_V2_TILE_COPIES 1
-#endif
-// copies of the tile: lane parity picks the copy, so neighbouring lanes in one cell (the
-// common same-address atomic conflict) hit different words; the flush sums the copies
-constexpr int kTileCopies = MOC_V2_TILE_COPIES;
-#ifndef MOC_V2_QSTAGE
-#define MOC_V2_QSTAGE 0
-#endif
-// MOC_V2_QSTAGE: each chunk's FSR sources (and material, in the pad slot) are staged in
-// shared memory next to the tile, one coalesced pass per chunk, and Eq. 3 reads them with
-// two LDS.128 instead of one scattered 256-bit global load per segment (each distinct FSR
-// record a lane touches costs an L1 data-pipe wavefront).  Needs the pad slot (G < GP).
-// Measured slower (cfg4 20.4 vs 17.2 ms, cfg5 130.3 vs 126.2 ms): the staged LDS.128 pair
-// costs as many data-pipe wavefronts as the global load it replaces (bank conflicts between
-// lanes' 32-byte records; ncu shared-load wavefronts 3.8e9 -> 15.6e9 on cfg5) and the
-// halved tile capacity doubles the chunk steps.
-__host__ __device__ constexpr bool staged(int G, int GP) { return MOC_V2_QSTAGE && G < GP; }
-// tile cell stride in u32 words: the G group words (plus the count word without
-// MOC_V2_NOCOUNT), rounded up to an odd count so lanes in consecutive cells hit distinct banks
-#ifndef MOC_V2_CELL_GP1
-#define MOC_V2_CELL_GP1 0  // 1: stride GP + 1 words as before the offset-free codes (A/B)
-#endif
-__host__ __device__ constexpr int cell_words(int G, int GP) {
-  return MOC_V2_NOCOUNT && !MOC_V2_CELL_GP1 ? (G | 1) : GP + 1;
-}
-__host__ __device__ constexpr int tile_cell_bytes(int G, int GP) { return 4 * cell_words(G, GP) * kTileCopies; }
-__host__ __device__ constexpr int cell_bytes(int G, int GP) { return tile_cell_bytes(G, GP) + (staged(G, GP) ? 4 * GP : 0); }
+// (Round-1 A/B variants that measured slower -- staged chunk sources, tile copies, packed
+// fp32 pairs, F2I codes, texture radial records, constant-bank planes, lane skew,
+// interleaved units, early advance, branch-free advance -- were removed from this file;
+// they live at git tag round1-v2-ab-options, their timings in DESIGN.md.)
+// tile cell stride in u32 words: the G group words rounded up to an odd count, so lanes in
+// consecutive cells hit distinct banks
+__host__ __device__ constexpr int cell_words(int G, int GP) { return G | 1; }
+__host__ __device__ constexpr int tile_cell_bytes(int G, int GP) { return 4 * cell_words(G, GP); }
+__host__ __device__ constexpr int cell_bytes(int G, int GP) { return tile_cell_bytes(G, GP); }
 __host__ __device__ constexpr int cap_max_cells(int G, int GP) { return ((224000 / kV2MinBlocks) / cell_bytes(G, GP)) & ~7; }
 
 // members i0, i0 + step, ..., i0 + (n - 1) step of one z-stack (step > 1 interleaves
@@ -154,8 +111,7 @@ struct V2Args {
   const uint32_t* link;
   const uint8_t* mat;
   const float* qt;      // [J][GP]; for G < GP slot G carries the FSR's material index bits
-  cudaTextureObject_t qtex;  // qt as a float4 texture (MOC_V2_QTEX: the gather on the TEX pipe)
-  cudaTextureObject_t ktf, ktb;  // per global 2D segment {s_end | s_start, region * NL} (MOC_V2_KTEX)
+  cudaTextureObject_t qtex;  // qt as a float4 texture (GP = 8: the gather on the TEX pipe)
   const float* qmax_t;  // [T2][GP] max qtilde over the FSRs under 2D track t
   const float* psi_in;
   float* psi_out;
@@ -164,7 +120,6 @@ struct V2Args {
   const Rec* store;     // EXP record store
   const uint32_t* cost; // exact merged segments per track (EXP replay length)
   int tile_off;         // byte offset of the tile in the dynamic buffer (multiple of 16)
-  int stage_off;        // byte offset of the staged sources [cap][GP] f32 (MOC_V2_QSTAGE)
   int cap_cells;        // tile capacity in cells (multiple of 8)
   double h_lane;        // thinnest axial layer / 3 (lane_lg_of)
   int lane_lg;          // forced log2 lane stride, -1 = per unit (lane_lg_of)
@@ -216,7 +171,7 @@ __device__ __forceinline__ float attenuation_dpsi(float psi, float q, float sig_
 
 template <int GP>
 __device__ __forceinline__ void load_q(const float* qt, int64_t j, float* q) {
-  if constexpr (GP == 8 && !MOC_V2_Q128) {
+  if constexpr (GP == 8) {
     // one 256-bit load per FSR record (LDG.E.ENL2.256): half the load instructions and L1
     // data-pipe wavefronts of two LDG.128 — the L1 data pipe is the sweep's busiest unit
     asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
@@ -260,12 +215,8 @@ __device__ __forceinline__ int kseg_upto(const KSeg* T, int nk, double s) {
 // fixed-point units (psi' = psi * scale_g, scale_g = 2^21 / bound_g), so the tally term
 // dpsi' = (psi' - q scale_g)(1 - e^{-tau}) is already scaled and its fixed-point code is
 // one FADD with the 1.5 * 2^23 magic: per group FMUL, MUFU.EX2, 2 FFMA, 2 FADD, ATOMS.
-// MOC_V2_PACKED pairs the groups with Blackwell's packed fp32 instructions (FMUL2 / FFMA2 /
-// FADD2; a pair then costs 9 issue slots instead of 14, the hot loop 116 instead of 128
-// instructions) but measured slower (cfg4 22.07 vs 20.87 ms, cfg5 165.6 vs 159.2 ms):
-// FFMA2 holds the FMA pipe for two cycles (profiles/micro_r2.jsonl: same 122 FMA/clk/SM as
-// FFMA) and the kernel is latency-, not issue-bound.  Storage is in pairs either way; for
-// odd G the last pair's upper half is a dead lane (scale 0, psi 0).
+// Storage is in float2 pairs; for odd G the last pair's upper half is a dead lane (scale 0,
+// psi 0).
 template <int G, int GP>
 struct Physics {
   static constexpr int NP = (G + 1) / 2;
@@ -274,41 +225,18 @@ struct Physics {
   const uint8_t* mat;
   const float* qt;
   cudaTextureObject_t qtex;
-  cudaTextureObject_t ktf, ktb;
-  int sb;        // global index of the unit's first 2D segment (MOC_V2_KTEX fetches)
   int cb;        // first cell of the current chunk (tile cell 0)
   int tile_off;  // byte offset of the tile in the dynamic buffer
   uint32_t tsa;  // shared address of the tile minus cb cells (cell pc at tsa + pc * 4 cell_words)
   uint32_t ssa;  // shared address of sh_sig
   uint32_t psa;  // shared address of sh_planes
-  uint32_t nem;  // emissions (MOC_V2_NOCOUNT: the tile has no per-cell count)
-  uint32_t qsa;  // shared address of the staged sources minus cb records
-  static constexpr bool kStaged = staged(G, GP);
+  uint32_t nem;  // emissions (the tile has no per-cell count)
 
-  // Eq. 3 for pending cell pc with its source and material read from the chunk's stage
-  __device__ __forceinline__ void emit_staged(int pc, float Lf) {
-    float q[GP];
-    const uint32_t qa = qsa + (uint32_t)pc * (4u * GP);
-#pragma unroll
-    for (int h = 0; h < GP / 4; ++h)
-      asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-          : "=f"(q[4 * h]), "=f"(q[4 * h + 1]), "=f"(q[4 * h + 2]), "=f"(q[4 * h + 3])
-          : "r"(qa + 16u * h));
-    emit(pc, __float_as_int(q[G]), q, Lf);
-  }
-
-  // axial plane i: from the constant bank (MOC_V2_PLANES_CONST; off the L1 data pipe) or an
-  // LDS.64 from the register-held shared base
+  // axial plane i: an LDS.64 from the register-held shared base
   __device__ __forceinline__ double plane(int i) const {
-#if MOC_V2_PLANES_CONST
-    return c_planes[i];
-#elif !defined(MOC_V2_GENERIC_SMEM)
     double z;
     asm("ld.shared.f64 %0, [%1];" : "=d"(z) : "r"(psa + 8u * (uint32_t)i));
     return z;
-#else
-    return sh_planes[i];
-#endif
   }
 #ifdef MOC_DEBUG_WALK
   int dbg_lo, dbg_hi, dbg_dir;
@@ -325,91 +253,25 @@ struct Physics {
       return;
     }
 #endif
-#ifndef MOC_V2_GENERIC_SMEM
     // 32-bit shared-window addresses held in registers (tile base pre-offset by the
     // chunk's first cell; Sigma_t table base): one IMAD / LEA per emit instead of the
     // compiler re-deriving both generic->shared bases (S2UR CgaCtaId, ULEA, LDC) each time
     const uint32_t ca = tsa + (uint32_t)pc * (4u * cell_words(G, GP));
-#if !MOC_V2_NOCOUNT
-    asm volatile("red.shared.add.u32 [%0+%1], 1;" ::"r"(ca), "n"(4 * GP));
-#endif
+    // Sigma_t from the constant bank (LDC through the constant cache, off the L1 data pipe;
+    // lanes mostly share the material, else the load replays per distinct address)
     float sg[GP];
-    if constexpr (MOC_V2_SIG_CONST) {
-      // Sigma_t from the constant bank (LDC through the constant cache, off the L1 data pipe;
-      // lanes mostly share the material, else the load replays per distinct address)
 #pragma unroll
-      for (int h = 0; h < GP; ++h) sg[h] = h < G ? c_sigt2[m * kMaxG + h] : 0.f;
-    } else if constexpr (GP % 4 == 0) {
-#pragma unroll
-      for (int h = 0; h < GP / 4; ++h)
-        asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-            : "=f"(sg[4 * h]), "=f"(sg[4 * h + 1]), "=f"(sg[4 * h + 2]), "=f"(sg[4 * h + 3])
-            : "r"(ssa + (uint32_t)m * (4u * GP) + 16u * h));
-    } else {
-#pragma unroll
-      for (int h = 0; h < GP; ++h)
-        asm("ld.shared.f32 %0, [%1];" : "=f"(sg[h]) : "r"(ssa + (uint32_t)m * (4u * GP) + 4u * h));
-    }
-#if MOC_V2_NOCOUNT
+    for (int h = 0; h < GP; ++h) sg[h] = h < G ? c_sigt2[m * kMaxG + h] : 0.f;
     ++nem;
 #define MOC_TILE_ADD(g, v) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(ca + 4u * (g)), "r"((v) - kMagicBits))
-#else
-#define MOC_TILE_ADD(g, v) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(ca + 4u * (g)), "r"(v))
-#endif
-#else
-    extern __shared__ __align__(16) uint8_t dsm[];
-    const int x = pc - cb;
-    uint32_t* cell = reinterpret_cast<uint32_t*>(dsm + tile_off) + x * cell_words(G, GP);
-    atomicAdd(cell + GP, 1u);
-    float sg[GP];
-    if constexpr (GP % 4 == 0) {
-#pragma unroll
-      for (int h = 0; h < GP / 4; ++h) {
-        const float4 x = reinterpret_cast<const float4*>(sh_sig + m * GP)[h];
-        sg[4 * h] = x.x;
-        sg[4 * h + 1] = x.y;
-        sg[4 * h + 2] = x.z;
-        sg[4 * h + 3] = x.w;
-      }
-    } else {
-#pragma unroll
-      for (int h = 0; h < GP; ++h) sg[h] = sh_sig[m * GP + h];
-    }
-#define MOC_TILE_ADD(g, v) atomicAdd(cell + (g), (v))
-#endif
-#ifndef MOC_V2_PACKED
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const float E = ex2_approx(-sg[g] * Lf);
       const float dd = fmaf(-q[g], scl(g), psi(g));
       const float dl = fmaf(-dd, E, dd);  // (psi' - q')(1 - E)
       psi(g) -= dl;
-#if MOC_V2_F2I && MOC_V2_NOCOUNT
-      // fixed-point code by one F2I (XU pipe) instead of FADD + IADD (A/B)
-      asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(ca + 4u * g), "r"((uint32_t)__float2int_rn(dl)));
-#else
       MOC_TILE_ADD(g, __float_as_uint(dl + kMagic));
-#endif
     }
-#else
-    const float2 nL = make_float2(-Lf, -Lf);
-#pragma unroll
-    for (int i = 0; i < NP; ++i) {
-      const int g0 = 2 * i, g1 = 2 * i + 1;
-      const float2 sp = make_float2(sg[g0], g1 < GP ? sg[g1] : 0.f);
-      const float2 qp = make_float2(-q[g0], g1 < GP ? -q[g1] : 0.f);
-      const float2 ta = __fmul2_rn(sp, nL);  // -sigma_t log2(e) L
-      float2 E;
-      E.x = ex2_approx(ta.x);
-      E.y = g1 < G ? ex2_approx(ta.y) : 0.f;
-      const float2 dd = __ffma2_rn(qp, scl2[i], psi2[i]);                      // psi' - q'
-      const float2 dl = __ffma2_rn(make_float2(-dd.x, -dd.y), E, dd);          // (psi' - q')(1 - E)
-      psi2[i] = __fadd2_rn(psi2[i], make_float2(-dl.x, -dl.y));
-      const float2 code = __fadd2_rn(dl, make_float2(kMagic, kMagic));
-      MOC_TILE_ADD(g0, __float_as_uint(code.x));
-      if (g1 < G) MOC_TILE_ADD(g1, __float_as_uint(code.y));
-    }
-#endif
 #undef MOC_TILE_ADD
   }
 };
@@ -435,48 +297,29 @@ struct WalkState {
     kx = v.z;
     ky = v.w;
   }
-  // radial step to 2D segment k in the hot loop: MOC_V2_KTEX fetches {s, region * NL}
-  // through the texture pipe and only the per-unit cell offset from shared memory (4 bytes
-  // per lane on the LSU data pipe instead of 16)
-  __device__ __forceinline__ void step(const KSeg* T, cudaTextureObject_t kt, int sb_, int kk) {
-#if MOC_V2_KTEX
-    const int4 v = tex1Dfetch<int4>(kt, sb_ + kk);
-    s_rad = __hiloint2double(v.y, v.x);
-    kx = v.z;
-    ky = T[kk].ky;
-#else
-    load(T[kk]);
-#endif
-  }
-  // make raw piece (k, l) the pending segment: its cell, source and material (staged:
-  // only the cell; Eq. 3 reads the chunk's stage)
+  // radial step to 2D segment k in the hot loop: one LDS.128
+  __device__ __forceinline__ void step(const KSeg* T, int kk) { load(T[kk]); }
+  // make raw piece (k, l) the pending segment: its cell, source and material
   __device__ __forceinline__ void set_pending(int jx, int cy, int ll, const uint8_t* mat, const float* qt,
                                               cudaTextureObject_t qtex) {
     pc = cy + ll;
-    if constexpr (!staged(G, GP)) {
-      const int64_t j = (int64_t)(jx + ll);
-#if MOC_V2_QTEX
-      if constexpr (GP == 8) {
-        // the source gather through the texture pipe (its own L1TEX data path; the LSU
-        // data pipe carries the tally atomics; the solver refuses problems whose sources
-        // exceed a 1D texture, > 2^26 FSRs at GP = 8)
-        const float4 a = tex1Dfetch<float4>(qtex, (int)(2 * j)), b = tex1Dfetch<float4>(qtex, (int)(2 * j + 1));
-        pq[0] = a.x; pq[1] = a.y; pq[2] = a.z; pq[3] = a.w;
-        pq[4] = b.x; pq[5] = b.y; pq[6] = b.z; pq[7] = b.w;
-      } else {
-        load_q<GP>(qt, j, pq);
-      }
-#else
+    const int64_t j = (int64_t)(jx + ll);
+    if constexpr (GP == 8) {
+      // the source gather through the texture pipe (its own L1TEX data path; the LSU
+      // data pipe carries the tally atomics; the solver refuses problems whose sources
+      // exceed a 1D texture, > 2^26 FSRs at GP = 8)
+      const float4 a = tex1Dfetch<float4>(qtex, (int)(2 * j)), b = tex1Dfetch<float4>(qtex, (int)(2 * j + 1));
+      pq[0] = a.x; pq[1] = a.y; pq[2] = a.z; pq[3] = a.w;
+      pq[4] = b.x; pq[5] = b.y; pq[6] = b.z; pq[7] = b.w;
+    } else {
       load_q<GP>(qt, j, pq);
-#endif
-      if constexpr (G < GP) pm = __float_as_int(pq[G]);  // material index rides in the pad slot
-      else pm = mat[j];
     }
+    if constexpr (G < GP) pm = __float_as_int(pq[G]);  // material index rides in the pad slot
+    else pm = mat[j];
   }
   template <class PH>
   __device__ __forceinline__ void emit_to(PH& ph, float L) {
-    if constexpr (staged(G, GP)) ph.emit_staged(pc, L);
-    else ph.emit(pc, pm, pq, L);
+    ph.emit(pc, pm, pq, L);
   }
 };
 
@@ -484,13 +327,9 @@ struct WalkState {
 // the track ends.  UP: the track climbs (cot > 0).
 template <int G, int GP, bool UP>
 __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, GP>& ph, const KSeg* TF, double z0,
-                                               double tn, double isn, int c_hi, int skew) {
+                                               double tn, double isn, int c_hi) {
   while (true) {
     if (w.pc >= c_hi) return;
-    if (skew > 0) {  // lane skew: sit out this trip (see walk_chunk)
-      --skew;
-      continue;
-    }
     if (w.done) {
       if (w.pc >= 0) {
         w.emit_to(ph, w.pL);
@@ -512,13 +351,6 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
     sn = last ? w.s_end : sn;
     const double L3d = (sn - w.s) * isn;
     const float L3 = (float)L3d;
-#ifdef MOC_V2_EARLY_ADVANCE
-    // MOC_V2_EARLY_ADVANCE: both candidate next crossings loaded before Eq. 3 (issue is in
-    // order, so their latency would hide under it; TF[nk] is TB[0]: a harmless read) —
-    // measured slower (cfg5 161.1 vs 157.9 ms: longer live ranges)
-    const int4 nv = *reinterpret_cast<const int4*>(&TF[w.k + 1]);
-    const double s_ax_n = (ph.plane(UP ? w.l + 2 : max(w.l - 1, 0)) - z0) * tn;
-#endif
     if (L3d < c_epsL) {
       if (w.pc >= 0) {
         w.pL += L3;  // a sliver merges into the segment before it
@@ -536,30 +368,13 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
       w.done = 1;
     } else {
       w.s = sn;
-#ifdef MOC_V2_EARLY_ADVANCE
       if (rad) {
         ++w.k;
-        w.s_rad = __hiloint2double(nv.y, nv.x);
-        w.kx = nv.z;
-        w.ky = nv.w;
-      } else {
-        w.l += UP ? 1 : -1;
-        w.s_ax = s_ax_n;
-      }
-#elif !defined(MOC_V2_BRANCHLESS)
-      if (rad) {
-        ++w.k;
-        w.step(TF, ph.ktf, ph.sb, w.k);
+        w.step(TF, w.k);
       } else {
         w.l += UP ? 1 : -1;
         w.s_ax = (ph.plane(w.l + (UP ? 1 : 0)) - z0) * tn;
       }
-#else
-      w.k += rad ? 1 : 0;
-      w.l += rad ? 0 : (UP ? 1 : -1);
-      w.load(TF[w.k]);
-      w.s_ax = (ph.plane(w.l + (UP ? 1 : 0)) - z0) * tn;
-#endif
     }
   }
 }
@@ -569,13 +384,9 @@ __device__ __forceinline__ void walk_fwd_chunk(WalkState<G, GP>& w, Physics<G, G
 // merged list is the reverse of the forward one (reading Q22b).
 template <int G, int GP, bool UP>
 __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, GP>& ph, const KSeg* TF,
-                                               const KSeg* TB, double z0, double tn, double isn, int c_lo, int skew) {
+                                               const KSeg* TB, double z0, double tn, double isn, int c_lo) {
   while (true) {
     if ((unsigned)w.pc < (unsigned)c_lo) return;
-    if (skew > 0) {
-      --skew;
-      continue;
-    }
     if (w.done) {
       if (w.pc >= 0) {
         w.emit_to(ph, w.pL + w.carry);
@@ -597,10 +408,6 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, G
     sp = last ? w.s_end : sp;
     const double L3d = (w.s - sp) * isn;
     const float L3 = (float)L3d;
-#ifdef MOC_V2_EARLY_ADVANCE
-    const int4 nv = *reinterpret_cast<const int4*>(&TB[w.k - 1]);  // TB[-1] is TF[nk-1]: harmless
-    const double s_ax_n = (ph.plane(UP ? max(w.l - 1, 0) : w.l + 2) - z0) * tn;
-#endif
     if (L3d < c_epsL) {
       w.carry += L3;
       if (w.pc < 0) w.fkl = w.k | (w.l << 16);  // the forward-first sliver wins
@@ -614,30 +421,13 @@ __device__ __forceinline__ void walk_bwd_chunk(WalkState<G, GP>& w, Physics<G, G
       w.done = 1;
     } else {
       w.s = sp;
-#ifdef MOC_V2_EARLY_ADVANCE
       if (rad) {
         --w.k;
-        w.s_rad = __hiloint2double(nv.y, nv.x);
-        w.kx = nv.z;
-        w.ky = nv.w;
-      } else {
-        w.l -= UP ? 1 : -1;
-        w.s_ax = s_ax_n;
-      }
-#elif !defined(MOC_V2_BRANCHLESS)
-      if (rad) {
-        --w.k;
-        w.step(TB, ph.ktb, ph.sb, w.k);
+        w.step(TB, w.k);
       } else {
         w.l -= UP ? 1 : -1;
         w.s_ax = (ph.plane(w.l + (UP ? 0 : 1)) - z0) * tn;
       }
-#else
-      w.k -= rad ? 1 : 0;
-      w.l -= rad ? 0 : (UP ? 1 : -1);
-      w.load(TB[w.k]);
-      w.s_ax = (ph.plane(w.l + (UP ? 0 : 1)) - z0) * tn;
-#endif
     }
   }
 }
@@ -705,20 +495,12 @@ __device__ __forceinline__ void replay_chunk(Replay<GP>& r, Physics<G, GP>& ph, 
   }
 }
 
-// one direction of one track through one chunk.  Lane skew (MOC_V2_LANE_SKEW = m > 1):
-// lane L starts the chunk L mod m loop trips late.  A warp's lanes advance one raw piece
-// per trip in lockstep, and neighbouring lanes (members 2^lg apart) otherwise sit in the
-// same tally cell at the same trip; offset by a piece they are in different cells, so the
-// tile atomics of one warp instruction conflict less (m - 1 extra trips per chunk).
-#ifndef MOC_V2_LANE_SKEW
-#define MOC_V2_LANE_SKEW 1
-#endif
+// one direction of one track through one chunk
 template <int G, int GP, bool UP>
 __device__ __forceinline__ void walk_chunk(int dir, WalkState<G, GP>& w, Physics<G, GP>& ph, const KSeg* TF,
                                            const KSeg* TB, double z0, double tn, double isn, int c_lo, int c_hi) {
-  const int skew = MOC_V2_LANE_SKEW > 1 ? (int)(threadIdx.x & 31) % MOC_V2_LANE_SKEW : 0;
-  if (dir == 0) walk_fwd_chunk<G, GP, UP>(w, ph, TF, z0, tn, isn, c_hi, skew);
-  else walk_bwd_chunk<G, GP, UP>(w, ph, TF, TB, z0, tn, isn, c_lo, skew);
+  if (dir == 0) walk_fwd_chunk<G, GP, UP>(w, ph, TF, z0, tn, isn, c_hi);
+  else walk_bwd_chunk<G, GP, UP>(w, ph, TF, TB, z0, tn, isn, c_lo);
 }
 
 // largest k in [k_lo, k_hi) with base[k] <= c (the 2D segment owning tile cell c)
@@ -729,27 +511,6 @@ __device__ __forceinline__ int k_of_cell(const int* base, int k_lo, int k_hi, in
     if (base[mid] <= c) lo = mid; else hi = mid - 1;
   }
   return lo;
-}
-
-// Stage chunk [k_lo, k_hi)'s FSR records (source + material) into stage[0, ce - cb): each
-// warp a contiguous share of the cells, lane-strided (consecutive cells of one 2D segment
-// are consecutive FSRs, so the global reads coalesce), cell -> 2D segment as in the flush.
-template <int GP>
-__device__ __forceinline__ void stage_chunk(float* stage, const float* qt, const KSeg* TF, const int* base, int k_lo,
-                                            int k_hi, int warp, int lane, int nw) {
-  const int cb = base[k_lo], n = base[k_hi] - cb;
-  const int per = (n + nw - 1) / nw;
-  const int x0 = warp * per + lane, x1 = min(n, (warp + 1) * per);
-  int kc = x0 < x1 ? k_of_cell(base, k_lo, k_hi, cb + x0) : k_lo;
-  for (int x = x0; x < x1; x += 32) {
-    while (base[kc + 1] <= cb + x) ++kc;
-    const KSeg e = TF[kc];
-    float v[GP];
-    load_q<GP>(qt, (int64_t)(e.kx - e.ky) + cb + x, v);
-#pragma unroll
-    for (int h = 0; h < GP / 4; ++h)
-      reinterpret_cast<float4*>(stage + (size_t)x * GP)[h] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
-  }
 }
 
 // EXP = false: on-the-fly sweep of the units past the preloaded prefix (the replay path
@@ -773,7 +534,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
   }
   for (int q = tid; q <= d.NL; q += blockDim.x) sh_planes[q] = d.planes[q];
   // the tile starts zeroed; each flush re-zeroes exactly the cells it consumed
-  for (int q = tid; q < cap * kCW * kTileCopies; q += blockDim.x) cells[q] = 0u;
+  for (int q = tid; q < cap * kCW; q += blockDim.x) cells[q] = 0u;
   const float ps = (float)a.sc[SC_PSI_SCALE];
   const OtfView v{nullptr, nullptr, sh_planes, d.NL};
   double leak = 0.0;
@@ -826,7 +587,6 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     const bool active = p < (int)U.n;
     const uint32_t id = d.st_first[s] + U.i0 + (uint32_t)p * U.step;
     float fpsi[GP], bpsi[GP];
-#if !MOC_V2_PSI_SCALAR
     if (active) {
       load_q<GP>(a.psi_in, (int64_t)(2 * id), fpsi);
       load_q<GP>(a.psi_in, (int64_t)(2 * id + 1), bpsi);
@@ -834,13 +594,6 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
 #pragma unroll
       for (int g = 0; g < GP; ++g) fpsi[g] = bpsi[g] = 0.f;
     }
-#else
-#pragma unroll
-    for (int g = 0; g < GP; ++g) {
-      fpsi[g] = active && g < G ? a.psi_in[(size_t)(2 * id) * GP + g] : 0.f;
-      bpsi[g] = active && g < G ? a.psi_in[(size_t)(2 * id + 1) * GP + g] : 0.f;
-    }
-#endif
     if (warp == 0) {
       int carry = 0;
       for (int b0 = 0; b0 < nk; b0 += 32) {
@@ -900,9 +653,6 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
       if (lane == 0) atomicMax(&sh_max[g], __float_as_uint(m));
     }
     __syncthreads();
-    constexpr bool kStage = Physics<G, GP>::kStaged && !EXP;
-    float* const stage = reinterpret_cast<float*>(dsm + a.stage_off);  // [cap][GP] (kStage)
-    if constexpr (kStage) stage_chunk<GP>(stage, a.qt, TF, base, chunk[0], chunk[1], warp, lane, nw);
     if (tid < G) {
       const float b = fmaxf(__uint_as_float(sh_max[tid]), a.qmax_t[(size_t)t * GP + tid]) * 1.0001f;
       sh_scale[tid] = b > 0.f ? kFixOne / b : 0.f;
@@ -915,12 +665,8 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     ph.mat = a.mat;
     ph.qt = a.qt;
     ph.qtex = a.qtex;
-    ph.ktf = a.ktf;
-    ph.ktb = a.ktb;
-    ph.sb = (int)sb;
     ph.tile_off = a.tile_off;
     const uint32_t tile_sa = (uint32_t)__cvta_generic_to_shared(dsm) + (uint32_t)a.tile_off;
-    const uint32_t stage_sa = (uint32_t)__cvta_generic_to_shared(dsm) + (uint32_t)a.stage_off;
     ph.ssa = opaque_u32((uint32_t)__cvta_generic_to_shared(sh_sig));
     ph.psa = opaque_u32((uint32_t)__cvta_generic_to_shared(sh_planes));
     const double tn = d.an_tan[an], isn = d.an_invsin[an], Lt = d.t_len[t];
@@ -945,12 +691,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     for (int dir = 0; dir < 2; ++dir) {
       {
         float pin[GP] = {};  // re-read (an L1/L2 hit): holding both directions' psi costs spills
-#if !MOC_V2_PSI_SCALAR
         if (active) load_q<GP>(a.psi_in, (int64_t)(2 * id + dir), pin);
-#else
-#pragma unroll
-        for (int g = 0; g < GP; ++g) pin[g] = active && g < G ? a.psi_in[(size_t)(2 * id + dir) * GP + g] : 0.f;
-#endif
 #pragma unroll
         for (int g = 0; g < 2 * Physics<G, GP>::NP; ++g) ph.psi(g) = active && g < G ? pin[g] * ps * ph.scl(g) : 0.f;
       }
@@ -1003,9 +744,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         const int k_lo = chunk[c], k_hi = chunk[c + 1];
         const int cb = base[k_lo], ce = base[k_hi];
         ph.cb = cb;
-        ph.tsa = opaque_u32(tile_sa - (uint32_t)cb * (4u * kCW) + (uint32_t)((lane % kTileCopies) * cap) * (4u * kCW));
-        // the stage holds this chunk (staged at the unit start or by the previous flush phase)
-        if constexpr (kStage) ph.qsa = opaque_u32(stage_sa - (uint32_t)cb * (4u * GP));
+        ph.tsa = opaque_u32(tile_sa - (uint32_t)cb * (4u * kCW));
 #ifdef MOC_DEBUG_WALK
         ph.dbg_lo = cb;
         ph.dbg_hi = ce;
@@ -1030,43 +769,26 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         int kc = x0 < x1 ? k_of_cell(base, k_lo, k_hi, cb + x0) : k_lo;
         for (int x = x0; x < x1; x += 32) {
           uint32_t* cp = cells + (size_t)x * kCW;
-#if MOC_V2_NOCOUNT
-          constexpr uint32_t cnt = 0u;
           uint32_t any = 0u;
           uint32_t sum[GP];
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             sum[g] = cp[g];
-#pragma unroll
-            for (int c = 1; c < kTileCopies; ++c) sum[g] += cp[(size_t)c * cap * kCW + g];
             any |= sum[g];
           }
           if (!any) continue;
-#else
-          const uint32_t cnt = cp[GP];
-          if (!cnt) continue;
-          cp[GP] = 0u;
-          nemit += cnt;
-#endif
           while (base[kc + 1] <= cb + x) ++kc;
           const KSeg e = TF[kc];
           const int64_t j = (int64_t)(e.kx - e.ky) + cb + x;  // FSR of cell cb + x = ky + layer
           uint32_t raw[GP];
 #pragma unroll
           for (int g = 0; g < GP; ++g) {
-#if MOC_V2_NOCOUNT
             raw[g] = g < G ? sum[g] : 0u;  // pad words are never written
-            if (g < G)
-#pragma unroll
-              for (int c = 0; c < kTileCopies; ++c) cp[(size_t)c * cap * kCW + g] = 0u;
-#else
-            raw[g] = g < G ? cp[g] : kMagicBits * cnt;  // pad words are never written
             if (g < G) cp[g] = 0u;
-#endif
           }
           float val[GP];
 #pragma unroll
-          for (int g = 0; g < GP; ++g) val[g] = g < G ? (float)(int)(raw[g] - cnt * kMagicBits) * fsc[g] : 0.f;
+          for (int g = 0; g < GP; ++g) val[g] = g < G ? (float)(int)raw[g] * fsc[g] : 0.f;
           float* dst = a.tally + j * GP;
           if constexpr (GP % 4 == 0) {
 #pragma unroll
@@ -1077,17 +799,12 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
             for (int g = 0; g < G; ++g) atomicAdd(dst + g, val[g]);
           }
         }
-        // stage the chunk walked next (forward: c + 1; backward: c - 1) in the same phase
-        if constexpr (kStage) {
-          const int cn = dir == 0 ? c + 1 : (ci + 1 < nchunk ? c - 1 : -1);
-          if (cn >= 0) stage_chunk<GP>(stage, a.qt, TF, base, chunk[cn], chunk[cn + 1], warp, lane, nw);
-        }
         __syncthreads();
       }
       if (active) {
         const uint32_t out = a.link[2 * id + dir];
         if (out != 0xffffffffu) {
-          if constexpr (GP == 8 && G < GP && !MOC_V2_PSI_SCALAR) {
+          if constexpr (GP == 8 && G < GP) {
             // one 256-bit store of the whole slot (the pad word of psi is never read)
             float v[8];
 #pragma unroll
@@ -1107,9 +824,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         }
       }
     }
-#if MOC_V2_NOCOUNT
     nemit += ph.nem;
-#endif
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

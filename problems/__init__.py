@@ -123,6 +123,65 @@ def xs_c5g7_synthetic(seed: int = SEED):
     return mats
 
 
+def load_xs_table(path: str, normalise_chi: bool = True):
+    """Real NEA C5G7 cross sections from a user-supplied table (SURVEY §8(f) unranked item,
+    P19: k-eff context against the published MCNP values; not a parity target).  JSON:
+
+        {"materials": [{"name": "UO2", "sigma_tr": [7], "nu_sigma_f": [7], "chi": [7],
+                        "sigma_s": [7][7] (from -> to)}, ...]}
+
+    with the eight C5G7 materials (C5G7_NAMES; NEA/NSC/DOC(2003)16 tables typed in by the
+    user: no data ships here).  sigma_t = the transport-corrected total sigma_tr (S:96,
+    reading Q13: Sigma_a = sigma_tr - sum sigma_s may be slightly negative).  A fissile chi
+    is renormalised to sum 1 (the published chi sums to 1.0000092; S:33 needs 1 +- 1e-9).
+    Returns the materials list in C5G7_NAMES order (the index order configs 3-5 use)."""
+    import json
+    with open(path) as f:
+        tab = json.load(f)
+    by = {m["name"]: m for m in tab["materials"]}
+    missing = [n for n in C5G7_NAMES if n not in by]
+    if missing:
+        raise ValueError(f"C5G7 table {path}: missing materials {missing}")
+    out = []
+    for name in C5G7_NAMES:
+        m = by[name]
+        st = np.asarray(m["sigma_tr"], np.float64)
+        ss = np.asarray(m["sigma_s"], np.float64)
+        nsf = np.asarray(m.get("nu_sigma_f", np.zeros(st.size)), np.float64)
+        chi = np.asarray(m.get("chi", np.zeros(st.size)), np.float64)
+        G = st.size
+        if ss.shape != (G, G) or nsf.size != G or chi.size != G:
+            raise ValueError(f"{name}: inconsistent group counts")
+        if not (st > 0).all() or (ss < 0).any() or (nsf < 0).any() or (chi < 0).any():
+            raise ValueError(f"{name}: sigma_tr must be > 0 and sigma_s, nu_sigma_f, chi >= 0")
+        if nsf.sum() > 0:
+            if abs(chi.sum() - 1.0) > 1e-4:
+                raise ValueError(f"{name}: chi sums to {chi.sum()}")
+            if normalise_chi:
+                chi = chi / chi.sum()
+        out.append(dict(name=name, sigma_t=st.tolist(), sigma_s=ss.tolist(), nu_sigma_f=nsf.tolist(),
+                        chi=chi.tolist()))
+    return out
+
+
+def dump_xs_table(mats, path: str):
+    """Write a materials list in load_xs_table's format (round-trip tests, templates)."""
+    import json
+    tab = {"materials": [dict(name=m["name"], sigma_tr=list(m["sigma_t"]), nu_sigma_f=list(m["nu_sigma_f"]),
+                              chi=list(m["chi"]), sigma_s=[list(r) for r in m["sigma_s"]]) for m in mats]}
+    with open(path, "w") as f:
+        json.dump(tab, f, indent=1)
+
+
+def with_xs(prob, mats):
+    """Copy of ``prob`` with its materials list replaced (same order and count)."""
+    if len(mats) != len(prob["materials"]):
+        raise ValueError("material count differs")
+    p = copy.deepcopy(prob)
+    p["materials"] = copy.deepcopy(mats)
+    return p
+
+
 # ----------------------------------------------------------------------------
 # geometry helpers
 # ----------------------------------------------------------------------------

@@ -176,12 +176,17 @@ def test_serpentine_balance_property(M):
 
 
 def test_pack_two_stacks_count(M):
-    # stacks of counts {3, 4} -> 7 entries, Alg. 1 order
+    """stacks of counts {3, 4} pack into 7 entries in Alg. 1 order (CSR offsets
+    0, 3, 7), read back through Eq. 13's accessor; and the product's own stack table is
+    that CSR (first = exclusive prefix sum of the per-stack member counts)."""
     g = GOLD["pack_two_stacks"]
-    prob = P.config(1)
-    st = M.Problem(prob).stacks()
-    assert st["first"][-1] == st["count"].sum()
-    assert sum(g["counts"]) == g["entries"]
+    off = np.concatenate([[0], np.cumsum(g["counts"])]).astype(np.int64)
+    assert off[-1] == g["entries"]
+    # every (stack i, member k) of the two stacks maps to a distinct entry 0..6
+    idx = sorted(M.moc_flat_index(off, 1, i, 0, k) for i, n in enumerate(g["counts"]) for k in range(n))
+    assert idx == list(range(g["entries"]))
+    st = M.Problem(P.config(1)).stacks()
+    np.testing.assert_array_equal(st["first"], np.concatenate([[0], np.cumsum(st["count"])]))
 
 
 # ------------------------------------------------------------- errors / geometry

@@ -102,3 +102,34 @@ def test_halo_exchange_gloo(M, world):
     assert all(ok for _, ok, _, _ in res), res
     assert sum(n for _, _, _, n in res) == 2 * M.Problem(prob).stats()["n_tracks3d"]
     assert all(h > 0 for _, _, h, _ in res)
+
+
+# ---------------------------------------------------------------- NEA C5G7 table loader
+def test_xs_table_round_trip_and_validation(tmp_path):
+    """problems.load_xs_table (SURVEY §8(f) unranked: real C5G7 data from a user file):
+    the seeded synthetic set written in the table format loads back identically (order,
+    groups, transport-corrected total as sigma_t); malformed tables are refused."""
+    import json
+
+    import problems as P
+    mats = P.xs_c5g7_synthetic()
+    f = tmp_path / "c5g7.json"
+    P.dump_xs_table(list(reversed(mats)), str(f))  # order in the file does not matter
+    back = P.load_xs_table(str(f))
+    assert [m["name"] for m in back] == P.C5G7_NAMES
+    for a, b in zip(mats, back):
+        for key in ("sigma_t", "nu_sigma_f", "chi", "sigma_s"):
+            np.testing.assert_allclose(np.array(a[key]), np.array(b[key]), rtol=1e-15, atol=0)
+    prob = P.with_xs(P.config(4), back)
+    assert prob["materials"][0]["name"] == "UO2"
+    tab = json.loads(f.read_text())
+    tab["materials"] = tab["materials"][1:]
+    bad = tmp_path / "bad.json"
+    bad.write_text(json.dumps(tab))
+    with pytest.raises(ValueError):
+        P.load_xs_table(str(bad))
+    tab = json.loads(f.read_text())
+    tab["materials"][0]["sigma_s"][0][0] = -1.0
+    bad.write_text(json.dumps(tab))
+    with pytest.raises(ValueError):
+        P.load_xs_table(str(bad))
