@@ -189,12 +189,14 @@ def test_cfg3_assembly_converged_parity(M, parity_log, schedule):
     ("cfg3_it12", lambda: P.config(3)),
     ("cfg4_it5", lambda: P.config(4)),
     ("cfg3_fine_it2", lambda: P.with_quadrature(P.config(3), radial_spacing=0.05, axial_spacing=0.1)),
+    ("cfg5_it2", lambda: P.config(5)),  # the benched configuration (SURVEY §8(c) fixed-N = 2)
 ])
 def test_full_size_fixed_iteration_golden(M, parity_log, case, make, schedule):
     """BASELINE sizes in the launch configuration bench.py times: k history and sampled
     FSR fluxes after N power iterations from phi = 1, k = 1, psi = 0 against the fp64
-    oracle (SURVEY §8(c) fixed-N parity: cfg4 N = 5).  cfg3_fine = the assembly at cfg5's
-    tracking (0.05 cm / 0.1 cm: dz = 0.10-0.28 cm, the v2 sweep's lane strides 4 and 8)."""
+    oracle (SURVEY §8(c) fixed-N parity: cfg4 N = 5, cfg5 N = 2).  cfg3_fine = the assembly
+    at cfg5's tracking (0.05 cm / 0.1 cm: dz = 0.10-0.28 cm, the v2 sweep's lane strides 4
+    and 8)."""
     g = _golden(case)
     s = M.Solver(M.Problem(make()), schedule=schedule)
     n = int(g["fixed_iters"])
