@@ -388,7 +388,7 @@ def main():
                     help="multi-rank exchange (default nccl when every rank has its own GPU, else gloo)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the closed-form k-eff error legs")
-    ap.add_argument("--exp", action="store_true", help="EXP/OTF hybrid of §4.2 instead of pure OTF")
+    ap.add_argument("--exp", action="store_true", help="EXP/OTF hybrid of §4.2 instead of pure OTF (--schedule 0)")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
     ap.add_argument("--xs", default=None, help="C5G7 cross-section table (problems.load_xs_table JSON)")
     args = ap.parse_args()

@@ -194,7 +194,7 @@ typedef struct {
   int32_t deterministic;    /* reserved (0) */
   int32_t tile_cells;       /* schedule 0: cap on FSR cells per shared-memory tally chunk
                                (0 = as many as fit; small values force many chunks, for tests) */
-  int32_t exp_mode;         /* schedule 0: 0 = pure on-the-fly (OTF); 1 = EXP/OTF hybrid of §4.2:
+  int32_t exp_mode;         /* schedule 0 only (else MOC_E_PARAM): 0 = pure on-the-fly (OTF); 1 = EXP/OTF hybrid of §4.2:
                                work units sorted by segment count descending are preloaded as stored
                                segments while the cumulative size stays within exp_fraction of the
                                budget, the rest is traced on the fly */

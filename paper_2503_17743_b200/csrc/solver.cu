@@ -1334,6 +1334,7 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     auto pol = thrust::cuda::par.on(st);
     int sched = s->opts.schedule;
     if (sched < 0 || sched > 3) throw Error(MOC_E_INVALID_ARG, "schedule must be 0, 1, 2 or 3");
+    if (s->opts.exp_mode != 0 && sched != 0) throw Error(MOC_E_PARAM, "exp_mode (EXP preload, §4.2) needs schedule 0");
     if (sched == 0) {
       // persistent stack-band units (sweep_v2.cuh), sorted by exact segment count descending
       int64_t max_nk = 0;

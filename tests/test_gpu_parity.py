@@ -126,12 +126,12 @@ def test_many_chunk_tiles_parity(M, oracle_mod, parity_log, tile_cells):
 
 @pytest.mark.parametrize("budget_mb", [0, 1])
 def test_exp_preload_parity(M, oracle_mod, parity_log, budget_mb):
-    """§4.2 EXP option: preloaded units replay stored segments in both
+    """§4.2 EXP option (schedule 0): preloaded units replay stored segments in both
     directions (budget 0 = everything that fits 80% of free memory, 1 MiB = hybrid).
     Same physics as OTF (S:348 mode equivalence): k and phi match the oracle and OTF."""
     prob = P.with_quadrature(P.config(3), num_azim=8, num_polar=4, radial_spacing=0.5, axial_spacing=3.0)
     pr = M.Problem(prob)
-    s = M.Solver(pr, exp_mode=1, exp_budget_mb=budget_mb)
+    s = M.Solver(pr, schedule=0, exp_mode=1, exp_budget_mb=budget_mb)
     t = s.timings()
     assert t["exp_segments"] > 0
     if budget_mb:
@@ -142,7 +142,7 @@ def test_exp_preload_parity(M, oracle_mod, parity_log, budget_mb):
     _check_emitted(s)
     ref = oracle_mod.Oracle(prob).solve(fixed_iters=3)
     _check(parity_log, f"cfg3_reduced_exp{budget_mb}", k, ref["k"], s.scalar_flux(), ref["phi"])
-    s0 = M.Solver(pr)
+    s0 = M.Solver(pr, schedule=0)
     k0, _ = s0.iterate(3)
     assert k == pytest.approx(k0, abs=1e-6)
 
