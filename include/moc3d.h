@@ -207,6 +207,13 @@ typedef struct {
                                 1, 2, 4 or 8 (0 = per unit from the stack's dz; for tests) */
   int32_t no_graph;          /* 1: launch every iteration's kernels individually instead of
                                 replaying a captured CUDA graph (debugging / A-B) */
+  int32_t gauss_seidel;      /* schedule 3, 5-7 groups, one GPU (not in the
+                                paper): one boundary-psi buffer updated in place, so a track whose
+                                linked predecessor was swept earlier in the same sweep starts from
+                                its fresh outgoing psi (asynchronous Gauss-Seidel along the 3D
+                                links) instead of last iteration's (Jacobi, Q9).  Halves the psi
+                                memory; the iterates differ (parity at convergence only), order
+                                and therefore results are not bitwise reproducible run to run */
 } moc_solver_opts;
 
 /* Upload the laydown to `device`, allocate HBM state (boundary psi double buffer,

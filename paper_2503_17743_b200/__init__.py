@@ -67,7 +67,7 @@ class moc_solver_opts(C.Structure):
                 ("deterministic", C.c_int32), ("tile_cells", C.c_int32), ("exp_mode", C.c_int32),
                 ("exp_budget_mb", C.c_int32), ("exp_fraction", C.c_double),
                 ("sc_lanes_per_cell", C.c_int32), ("sc_psi_cap", C.c_int32), ("v2_lane_stride", C.c_int32),
-                ("no_graph", C.c_int32)]
+                ("no_graph", C.c_int32), ("gauss_seidel", C.c_int32)]
 
 
 class moc_solve_opts(C.Structure):
@@ -335,7 +335,8 @@ class Solver:
     def __init__(self, problem: Problem, device: int = 0, stream=None, schedule: int = 3, threads: int = 0,
                  blocks: int = 0, rank: int = 0, world: int = 1, tile_cells: int = 0, exp_mode: int = 0,
                  exp_budget_mb: int = 0, exp_fraction: float = 0.0, sc_lanes_per_cell: int = 0,
-                 sc_psi_cap: int = 0, v2_lane_stride: int = 0, no_graph: bool = False, backend: str | None = None):
+                 sc_psi_cap: int = 0, v2_lane_stride: int = 0, no_graph: bool = False, backend: str | None = None,
+                 gauss_seidel: bool = False):
         """world > 1: one rank of a torch.distributed job.  backend "nccl"
         (default when the process group is NCCL): the library owns an NCCL communicator
         and runs the whole iteration on the device; "gloo": the exchange is staged through
@@ -351,7 +352,8 @@ class Solver:
             except Exception:  # torch without CUDA: legacy default stream
                 stream = 0
         opts = moc_solver_opts(schedule, threads, blocks, 0, tile_cells, exp_mode, exp_budget_mb, exp_fraction,
-                               sc_lanes_per_cell, sc_psi_cap, v2_lane_stride, int(bool(no_graph)))
+                               sc_lanes_per_cell, sc_psi_cap, v2_lane_stride, int(bool(no_graph)),
+                               int(bool(gauss_seidel)))
         comm = moc_comm_desc(rank, world, MOC_COMM_CALLER)
         if world > 1:
             import torch.distributed as dist

@@ -689,6 +689,7 @@ void run_sweep_sc(moc_solver* s, unsigned long long* hash = nullptr, int32_t* ns
   a.err = s->d_err;
   a.hash = hash;
   a.nseg = nseg;
+  a.gs = s->opts.gauss_seidel;
   k_sweep_sc<G, GP, HASH><<<HASH ? s->sc_blocks_hash : s->sc_blocks, kScThreads, HASH ? s->sc_smem_hash : s->sc_smem,
                             s->stream>>>(a);
 }
@@ -1040,7 +1041,8 @@ void reset_state(moc_solver* s) {
   const int nb = 1024;
   k_fill_f32<<<nb, 256, 0, s->stream>>>(s->d_phi, s->J * s->GP, 1.0f);
   CUDA_OK(cudaMemsetAsync(s->d_psi[0], 0, sizeof(float) * 2 * s->T3 * s->GP, s->stream));
-  CUDA_OK(cudaMemsetAsync(s->d_psi[1], 0, sizeof(float) * 2 * s->T3 * s->GP, s->stream));
+  if (s->d_psi[1] != s->d_psi[0])
+    CUDA_OK(cudaMemsetAsync(s->d_psi[1], 0, sizeof(float) * 2 * s->T3 * s->GP, s->stream));
   double sc[SC_N] = {0};
   sc[SC_K] = 1.0;
   sc[SC_PSI_SCALE] = 1.0;
@@ -1051,6 +1053,7 @@ void reset_state(moc_solver* s) {
 
 void destroy(moc_solver* s) {
   if (!s) return;
+  if (s->d_psi[1] == s->d_psi[0]) s->d_psi[1] = nullptr;  // Gauss-Seidel: one buffer
   void* ptrs[] = {s->d_seg_send, s->d_planes, s->d_t_len, s->d_seg_region, s->d_t_seg, s->d_t_a, s->d_an_cot,
                   s->d_an_tan, s->d_an_invsin, s->d_an_dz, s->d_an_vw, s->d_an_c, s->d_st_z0, s->d_st_first,
                   s->d_link, s->d_work, s->d_cost, s->d_mat, s->d_qt, s->d_phi, s->d_fold, s->d_fnew, s->d_tally,
@@ -1446,8 +1449,14 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
       s->sweep_blocks = s->opts.blocks > 0 ? s->opts.blocks : 512;
     }
     // --- state
+    if (s->opts.gauss_seidel) {
+      if (sched != 3 || !(s->GP == 8 && s->G < 8))
+        throw Error(MOC_E_PARAM, "gauss_seidel needs schedule 3 and 5-7 groups (the slot pad word holds the epoch)");
+      if (s->comm.world > 1) throw Error(MOC_E_PARAM, "gauss_seidel is single-GPU");
+    }
     s->d_psi[0] = dmalloc<float>(2 * (size_t)s->T3 * s->GP, B);
-    s->d_psi[1] = dmalloc<float>(2 * (size_t)s->T3 * s->GP, B);
+    // Jacobi: double buffer; Gauss-Seidel (NEXT-4): one buffer updated in place
+    s->d_psi[1] = s->opts.gauss_seidel ? s->d_psi[0] : dmalloc<float>(2 * (size_t)s->T3 * s->GP, B);
     for (auto& e : s->ev) CUDA_OK(cudaEventCreate(&e));
     reset_state(s);
   } catch (const Error& e) {

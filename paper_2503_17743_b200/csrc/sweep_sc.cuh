@@ -88,6 +88,7 @@ struct ScArgs {
   int* err;
   unsigned long long* hash;  // HASH: per slot FNV-1a of the emitted FSR ids, in travel order
   int32_t* nseg;             // HASH: per slot emitted segment count
+  int gs;                    // Gauss-Seidel (NEXT-4): psi_in == psi_out, slot pad word = write epoch
 };
 
 template <int G>
@@ -393,6 +394,7 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
       HASH ? reinterpret_cast<int*>(reinterpret_cast<uint64_t*>(hbase) + (size_t)kScWarps * pcap) + (size_t)warp * pcap
            : nullptr;
   const float ps = (float)a.sc[SC_PSI_SCALE];
+  const uint32_t ep = (uint32_t)a.sc[SC_ITER] + 1u;  // this sweep's epoch (Gauss-Seidel slots)
   double leak = 0.0;
   uint64_t nemit = 0;
 
@@ -427,10 +429,17 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
         const uint32_t id = id0 + (uint32_t)(mz ? B - 1 - m : m);
         float v[8];
         load_q<GP>(a.psi_in, (int64_t)(2 * id + dir), v);
+        // lazy normalisation: psi written in an earlier iteration is scaled on read; in
+        // Gauss-Seidel mode a slot already rewritten in this sweep (pad word = this epoch)
+        // is in the current units
+        float sc_ = ps;
+        if constexpr (GP == 8 && G < 8) {
+          if (a.gs && __float_as_uint(v[7]) == ep) sc_ = 1.f;
+        }
 #pragma unroll
         for (int h = 0; h < NH; ++h)
-          psl[h * pcap + m] = make_float4(v[4 * h] * ps, 4 * h + 1 < G ? v[4 * h + 1] * ps : 0.f,
-                                          4 * h + 2 < G ? v[4 * h + 2] * ps : 0.f, 4 * h + 3 < G ? v[4 * h + 3] * ps : 0.f);
+          psl[h * pcap + m] = make_float4(v[4 * h] * sc_, 4 * h + 1 < G ? v[4 * h + 1] * sc_ : 0.f,
+                                          4 * h + 2 < G ? v[4 * h + 2] * sc_ : 0.f, 4 * h + 3 < G ? v[4 * h + 3] * sc_ : 0.f);
         if constexpr (HASH) {
           hh[m] = kFnvInit;
           hc[m] = 0;
@@ -653,6 +662,9 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
         }
 #pragma unroll
         for (int g = G; g < 8; ++g) v[g] = 0.f;
+        if constexpr (GP == 8 && G < 8) {
+          if (a.gs) v[7] = __uint_as_float(ep);  // written in this sweep: current units
+        }
         const uint32_t out = a.link[2 * id + dir];
         if (out != 0xffffffffu) {
           float* dst = a.psi_out + (size_t)out * GP;
