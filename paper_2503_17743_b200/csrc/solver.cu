@@ -603,6 +603,9 @@ struct moc_solver {
   float *d_halo_send = nullptr, *d_halo_recv = nullptr;
   std::vector<int64_t> send_counts, recv_counts;  // per peer, in slots
   double owned_cost = 0;
+  uint32_t* d_slot_first = nullptr; // per stack: first track of this rank's numbering (world > 1)
+  int64_t T3_local = 0;             // tracks this rank sweeps (= T3 on one GPU)
+  int64_t psi_slots = 0;            // boundary-psi slots per buffer: 2 T3_local (+ halo send tail)
   ncclComm_t nccl = nullptr;        // backend MOC_COMM_NCCL: library-owned communicator
   moc_exchange_fn xfn = nullptr;    // backend MOC_COMM_CALLER: host exchange callback
   void* xctx = nullptr;
@@ -690,6 +693,7 @@ void run_sweep_sc(moc_solver* s, unsigned long long* hash = nullptr, int32_t* ns
   a.hash = hash;
   a.nseg = nseg;
   a.gs = s->opts.gauss_seidel;
+  a.slot_first = s->d_slot_first ? s->d_slot_first : s->d_st_first;
   k_sweep_sc<G, GP, HASH><<<HASH ? s->sc_blocks_hash : s->sc_blocks, kScThreads, HASH ? s->sc_smem_hash : s->sc_smem,
                             s->stream>>>(a);
 }
@@ -719,6 +723,7 @@ void run_sweep(moc_solver* s) {
     a.lane_lg = s->lane_lg;
     a.h_lane = s->h_lane;
     a.err = s->d_err;
+    a.slot_first = s->d_slot_first ? s->d_slot_first : s->d_st_first;
     a.unit_exp = s->d_unit_exp;
     a.store = s->d_store;
     a.cost = s->d_cost;
@@ -1040,9 +1045,9 @@ int padded_groups(int G) { return G <= 2 ? G : (G <= 4 ? 4 : 8); }
 void reset_state(moc_solver* s) {
   const int nb = 1024;
   k_fill_f32<<<nb, 256, 0, s->stream>>>(s->d_phi, s->J * s->GP, 1.0f);
-  CUDA_OK(cudaMemsetAsync(s->d_psi[0], 0, sizeof(float) * 2 * s->T3 * s->GP, s->stream));
+  CUDA_OK(cudaMemsetAsync(s->d_psi[0], 0, sizeof(float) * s->psi_slots * s->GP, s->stream));
   if (s->d_psi[1] != s->d_psi[0])
-    CUDA_OK(cudaMemsetAsync(s->d_psi[1], 0, sizeof(float) * 2 * s->T3 * s->GP, s->stream));
+    CUDA_OK(cudaMemsetAsync(s->d_psi[1], 0, sizeof(float) * s->psi_slots * s->GP, s->stream));
   double sc[SC_N] = {0};
   sc[SC_K] = 1.0;
   sc[SC_PSI_SCALE] = 1.0;
@@ -1060,7 +1065,7 @@ void destroy(moc_solver* s) {
                   s->d_vol, s->d_psi[0], s->d_psi[1], s->d_sc, s->d_part_a, s->d_part_b, s->d_part_c, s->d_hist,
                   s->d_units, s->d_counter, s->d_rmax, s->d_qmax_t, s->d_tally32, s->d_err,
                   s->d_unit_maxq, s->d_unit_exp, s->d_store, s->d_phi64, s->d_sc_units,
-                  s->d_send_slots, s->d_recv_slots, s->d_halo_send, s->d_halo_recv};
+                  s->d_send_slots, s->d_recv_slots, s->d_halo_send, s->d_halo_recv, s->d_slot_first};
   if (s->qtex) cudaDestroyTextureObject(s->qtex);
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1225,27 +1230,76 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
     {
       std::vector<int64_t> lk(2 * s->T3);
       links3d(g, L, lk.data());
-      std::vector<uint32_t> l32(2 * s->T3);
-      for (int64_t q = 0; q < 2 * s->T3; ++q) l32[q] = lk[q] < 0 ? 0xffffffffu : (uint32_t)lk[q];
-      s->d_link = dmalloc<uint32_t>(2 * s->T3, B);
-      upload(l32.data(), s->d_link, 4 * 2 * s->T3, st);
-      if (s->comm.world > 1) {
+      s->T3_local = s->T3;
+      s->psi_slots = 2 * s->T3;
+      if (s->comm.world <= 1) {
+        std::vector<uint32_t> l32(2 * s->T3);
+        for (int64_t q = 0; q < 2 * s->T3; ++q) l32[q] = lk[q] < 0 ? 0xffffffffu : (uint32_t)lk[q];
+        s->d_link = dmalloc<uint32_t>(2 * s->T3, B);
+        upload(l32.data(), s->d_link, 4 * 2 * s->T3, st);
+        CUDA_OK(cudaStreamSynchronize(st));
+      } else {
         if (s->opts.schedule != 0 && s->opts.schedule != 3)
           throw Error(MOC_E_PARAM, "multi-GPU runs use schedule 0 or 3");
         if (s->comm.rank < 0 || s->comm.rank >= s->comm.world) throw Error(MOC_E_INVALID_ARG, "bad rank");
         std::vector<double> cost;
         partition_stacks(L, s->comm.world, owner, &cost);
         s->owned_cost = cost[s->comm.rank];
+        const int rank = s->comm.rank, W = s->comm.world;
+        // this rank's track numbering: its stacks' members, in stack order (boundary psi is
+        // owned by the rank that sweeps the track)
+        std::vector<int64_t> loc(s->S + 1);
+        int64_t run = 0;
+        for (int64_t q = 0; q < s->S; ++q) {
+          loc[q] = run;
+          if (owner[q] == rank) run += L.st_cnt[q];
+        }
+        loc[s->S] = run;
+        s->T3_local = run;
+        auto stack_of = [&](int64_t gid) {
+          return (int64_t)(std::upper_bound(L.st_first.begin(), L.st_first.end(), gid) - L.st_first.begin() - 1);
+        };
+        auto local_slot = [&](int64_t gslot) {
+          const int64_t gid = gslot / 2, ts = stack_of(gid);
+          return 2 * (loc[ts] + (gid - L.st_first[ts])) + (gslot & 1);
+        };
         std::vector<std::vector<int64_t>> send, recv;
-        halo_plans(L, lk.data(), owner, s->comm.rank, s->comm.world, send, recv);
-        std::vector<uint32_t> ss, rr;
-        for (int p = 0; p < s->comm.world; ++p) {
+        halo_plans(L, lk.data(), owner, rank, W, send, recv);
+        std::vector<int64_t> soff(W + 1, 0);
+        for (int p = 0; p < W; ++p) {
           s->send_counts.push_back((int64_t)send[p].size());
           s->recv_counts.push_back((int64_t)recv[p].size());
-          for (int64_t x : send[p]) ss.push_back((uint32_t)x);
-          for (int64_t x : recv[p]) rr.push_back((uint32_t)x);
+          soff[p + 1] = soff[p] + (int64_t)send[p].size();
         }
-        s->n_send = (int64_t)ss.size();
+        s->n_send = soff[W];
+        s->psi_slots = 2 * s->T3_local + s->n_send;
+        // links in local slots: an owned target -> its local slot; another rank's target ->
+        // the next slot of the halo-send tail of its peer (source-slot order, the order of
+        // halo_plans and of the peer's receive list)
+        std::vector<uint32_t> l32(2 * s->T3_local, 0xffffffffu);
+        std::vector<int64_t> cnt(W, 0);
+        for (int64_t q = 0; q < s->S; ++q) {
+          if (owner[q] != rank) continue;
+          for (int64_t gid = L.st_first[q]; gid < L.st_first[q + 1]; ++gid)
+            for (int dd = 0; dd < 2; ++dd) {
+              const int64_t tgt = lk[2 * gid + dd];
+              const int64_t src = 2 * (loc[q] + (gid - L.st_first[q])) + dd;
+              if (tgt < 0) continue;
+              const int rt = owner[stack_of(tgt / 2)];
+              l32[src] = (uint32_t)(rt == rank ? local_slot(tgt) : 2 * s->T3_local + soff[rt] + cnt[rt]++);
+            }
+        }
+        s->d_link = dmalloc<uint32_t>(l32.size(), B);
+        upload(l32.data(), s->d_link, 4 * l32.size(), st);
+        std::vector<uint32_t> sf32(s->S + 1);
+        for (int64_t q = 0; q <= s->S; ++q) sf32[q] = (uint32_t)loc[q];
+        s->d_slot_first = dmalloc<uint32_t>(s->S + 1, B);
+        upload(sf32.data(), s->d_slot_first, 4 * (s->S + 1), st);
+        // halo: the send buffer is gathered from the tail; received psi scatter to local slots
+        std::vector<uint32_t> ss(s->n_send), rr;
+        for (int64_t x = 0; x < s->n_send; ++x) ss[x] = (uint32_t)(2 * s->T3_local + x);
+        for (int p = 0; p < W; ++p)
+          for (int64_t x : recv[p]) rr.push_back((uint32_t)local_slot(x));
         s->n_recv = (int64_t)rr.size();
         s->d_send_slots = dmalloc<uint32_t>(ss.size(), B);
         s->d_recv_slots = dmalloc<uint32_t>(rr.size(), B);
@@ -1253,6 +1307,7 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
         upload(rr.data(), s->d_recv_slots, 4 * rr.size(), st);
         s->d_halo_send = dmalloc<float>(ss.size() * s->GP, B);
         s->d_halo_recv = dmalloc<float>(rr.size() * s->GP, B);
+        CUDA_OK(cudaStreamSynchronize(st));
         if (s->comm.backend == MOC_COMM_NCCL) {
           static_assert(sizeof(ncclUniqueId) == sizeof(s->comm.nccl_id), "ncclUniqueId size");
           ncclUniqueId id;
@@ -1392,7 +1447,7 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
         size_t freeb = 0, totalb = 0;
         CUDA_OK(cudaMemGetInfo(&freeb, &totalb));
         // leave room for the boundary-psi double buffer allocated below
-        const double psi_bytes = 2.0 * 2.0 * (double)s->T3 * s->GP * sizeof(float);
+        const double psi_bytes = 2.0 * (double)s->psi_slots * s->GP * sizeof(float);
         double budget = s->opts.exp_budget_mb > 0 ? s->opts.exp_budget_mb * 1048576.0 : (double)freeb - psi_bytes;
         const double frac = s->opts.exp_fraction > 0 ? s->opts.exp_fraction : 0.8;
         const double lim = budget * frac;
@@ -1454,9 +1509,10 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
         throw Error(MOC_E_PARAM, "gauss_seidel needs schedule 3 and 5-7 groups (the slot pad word holds the epoch)");
       if (s->comm.world > 1) throw Error(MOC_E_PARAM, "gauss_seidel is single-GPU");
     }
-    s->d_psi[0] = dmalloc<float>(2 * (size_t)s->T3 * s->GP, B);
-    // Jacobi: double buffer; Gauss-Seidel (NEXT-4): one buffer updated in place
-    s->d_psi[1] = s->opts.gauss_seidel ? s->d_psi[0] : dmalloc<float>(2 * (size_t)s->T3 * s->GP, B);
+    // boundary psi of this rank's tracks (+ the halo-send tail); Jacobi: double buffer,
+    // Gauss-Seidel (NEXT-4): one buffer updated in place
+    s->d_psi[0] = dmalloc<float>((size_t)s->psi_slots * s->GP, B);
+    s->d_psi[1] = s->opts.gauss_seidel ? s->d_psi[0] : dmalloc<float>((size_t)s->psi_slots * s->GP, B);
     for (auto& e : s->ev) CUDA_OK(cudaEventCreate(&e));
     reset_state(s);
   } catch (const Error& e) {
@@ -1710,6 +1766,7 @@ int moc_sweep_checksums(moc_solver* s, int32_t* nseg, uint64_t* hash) {
   SOLVER_TRY(s, {
     CUDA_OK(cudaSetDevice(s->device));
     if (s->opts.schedule != 3) throw Error(MOC_E_STATE, "sweep checksums need schedule 3");
+    if (s->comm.world > 1) throw Error(MOC_E_STATE, "sweep checksums are single-GPU");
     ensure_constants(s);
     const size_t n = 2 * (size_t)s->T3;
     int64_t B = 0;

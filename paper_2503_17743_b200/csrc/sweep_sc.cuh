@@ -89,6 +89,7 @@ struct ScArgs {
   unsigned long long* hash;  // HASH: per slot FNV-1a of the emitted FSR ids, in travel order
   int32_t* nseg;             // HASH: per slot emitted segment count
   int gs;                    // Gauss-Seidel (NEXT-4): psi_in == psi_out, slot pad word = write epoch
+  const uint32_t* slot_first;  // per stack: first boundary-psi / link slot pair of its members on this rank
 };
 
 template <int G>
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
     const float dzf = (float)dz;
     const int B = (int)U.n, lgR = (int)U.lgR, R = 1 << lgR, C = 32 >> lgR;
     const bool up = cot > 0;
-    const uint32_t id0 = d.st_first[s] + U.i0;
+    const uint32_t id0 = a.slot_first[s] + U.i0;  // this rank's track numbering (psi, links)
     const float cw = d.an_c[an];
     const int ci = lane >> lgR, r = lane & (R - 1);
 

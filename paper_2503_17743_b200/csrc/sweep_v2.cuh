@@ -124,6 +124,7 @@ struct V2Args {
   double h_lane;        // thinnest axial layer / 3 (lane_lg_of)
   int lane_lg;          // forced log2 lane stride, -1 = per unit (lane_lg_of)
   int* err;
+  const uint32_t* slot_first;  // per stack: first psi / link slot pair of its members on this rank
 };
 
 // Stack member (within the unit's band) walked by thread tid, for a lane stride of
@@ -585,11 +586,12 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     //    psi loads are issued here so their HBM latency overlaps the scan below
     const int p = member_of(tid, lane_lg_of(dz * U.step, a.h_lane, a.lane_lg, (int)U.n));
     const bool active = p < (int)U.n;
-    const uint32_t id = d.st_first[s] + U.i0 + (uint32_t)p * U.step;
+    const uint32_t id = d.st_first[s] + U.i0 + (uint32_t)p * U.step;     // global track id (costs)
+    const uint32_t sid = a.slot_first[s] + U.i0 + (uint32_t)p * U.step;  // this rank's numbering (psi, links)
     float fpsi[GP], bpsi[GP];
     if (active) {
-      load_q<GP>(a.psi_in, (int64_t)(2 * id), fpsi);
-      load_q<GP>(a.psi_in, (int64_t)(2 * id + 1), bpsi);
+      load_q<GP>(a.psi_in, (int64_t)(2 * sid), fpsi);
+      load_q<GP>(a.psi_in, (int64_t)(2 * sid + 1), bpsi);
     } else {
 #pragma unroll
       for (int g = 0; g < GP; ++g) fpsi[g] = bpsi[g] = 0.f;
@@ -691,7 +693,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
     for (int dir = 0; dir < 2; ++dir) {
       {
         float pin[GP] = {};  // re-read (an L1/L2 hit): holding both directions' psi costs spills
-        if (active) load_q<GP>(a.psi_in, (int64_t)(2 * id + dir), pin);
+        if (active) load_q<GP>(a.psi_in, (int64_t)(2 * sid + dir), pin);
 #pragma unroll
         for (int g = 0; g < 2 * Physics<G, GP>::NP; ++g) ph.psi(g) = active && g < G ? pin[g] * ps * ph.scl(g) : 0.f;
       }
@@ -802,7 +804,7 @@ __global__ void __launch_bounds__(kV2Threads, kV2MinBlocks) k_sweep_v2(V2Args a)
         __syncthreads();
       }
       if (active) {
-        const uint32_t out = a.link[2 * id + dir];
+        const uint32_t out = a.link[2 * sid + dir];
         if (out != 0xffffffffu) {
           if constexpr (GP == 8 && G < GP) {
             // one 256-bit store of the whole slot (the pad word of psi is never read)
