@@ -355,6 +355,9 @@ class Solver:
                                sc_lanes_per_cell, sc_psi_cap, v2_lane_stride, int(bool(no_graph)),
                                int(bool(gauss_seidel)))
         comm = moc_comm_desc(rank, world, MOC_COMM_CALLER)
+        if world == 1 and backend == "nccl":  # 1-rank communicator (tests the NCCL path on one GPU)
+            comm.backend = MOC_COMM_NCCL
+            _check(L.moc_nccl_unique_id(comm.nccl_id), None, None)
         if world > 1:
             import torch.distributed as dist
             backend = backend or ("nccl" if dist.get_backend() == "nccl" else "gloo")

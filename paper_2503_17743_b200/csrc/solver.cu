@@ -843,7 +843,7 @@ void iter_finish_half(moc_solver* s) {
 // its tail) and the grouped point-to-point exchange of cut-crossing boundary psi, on the
 // solver's stream (NCCL), or through the caller's host callback.
 void exchange(moc_solver* s) {
-  if (s->comm.world <= 1) return;
+  if (s->comm.world <= 1 && !s->nccl) return;  // (a 1-rank NCCL communicator is a self-test)
   if (s->nccl) {
     NcclApi& n = nccl_api();
     const int GP = s->GP;
@@ -851,7 +851,7 @@ void exchange(moc_solver* s) {
     NCCL_OK(n.allReduce(s->d_tally32, s->d_tally32, (size_t)s->J * GP + 1, ncclFloat32, ncclSum, s->nccl,
                         s->stream));
     int64_t so = 0, ro = 0;
-    for (int p = 0; p < s->comm.world; ++p) {
+    for (int p = 0; p < (int)s->send_counts.size(); ++p) {
       if (s->send_counts[p])
         NCCL_OK(n.send(s->d_halo_send + so * GP, (size_t)(s->send_counts[p] * GP), ncclFloat32, p, s->nccl,
                        s->stream));
@@ -1238,6 +1238,11 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
         s->d_link = dmalloc<uint32_t>(2 * s->T3, B);
         upload(l32.data(), s->d_link, 4 * 2 * s->T3, st);
         CUDA_OK(cudaStreamSynchronize(st));
+        if (s->comm.backend == MOC_COMM_NCCL) {  // 1-rank communicator: exercises the NCCL path
+          ncclUniqueId id;
+          std::memcpy(&id, s->comm.nccl_id, sizeof(id));
+          NCCL_OK(nccl_api().commInitRank(&s->nccl, 1, id, 0));
+        }
       } else {
         if (s->opts.schedule != 0 && s->opts.schedule != 3)
           throw Error(MOC_E_PARAM, "multi-GPU runs use schedule 0 or 3");

@@ -112,3 +112,22 @@ def test_bench_two_ranks_gloo():
     assert len(d2["config"]["per_rank_ms"]) == 2
     assert d2["config"]["k_eff_after"] == pytest.approx(d1["config"]["k_eff_after"], abs=1e-6)
     assert d2["value"] > 0
+
+
+def test_nccl_path_single_rank():
+    """The in-library NCCL exchange on one GPU: libnccl.so.2 loaded at run time, a 1-rank
+    communicator, the tally all-reduce inside the captured CUDA graph of every iteration:
+    same k and flux as without it (the multi-GPU NCCL run itself needs one GPU per rank)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_17743_b200 as M
+    pr = M.Problem(P.small_lattice(3, 3, 4))
+    a, b = M.Solver(pr), M.Solver(pr, backend="nccl")
+    ka, _ = a.iterate(6)
+    kb, _ = b.iterate(6)
+    assert kb == pytest.approx(ka, abs=1e-7)
+    pa, pb = a.scalar_flux(), b.scalar_flux()
+    assert np.abs(pa - pb).max() / pa.max() < 1e-6
+    rb = b.solve(tol_k=1e-7, tol_src=1e-6, max_iter=3000)
+    assert rb["converged"]
