@@ -151,6 +151,15 @@ int moc_partition_exp_otf(const int64_t* estimates, int64_t n, double budget, do
 int moc_partition_stacks(const moc_problem* p, int32_t world, int32_t* owner, double* cost);
 int moc_halo_plan(const moc_problem* p, int32_t world, const int32_t* owner, int32_t rank, int32_t peer,
                   int64_t* slots, int64_t cap, int64_t* n);
+/* The layout the solver uses on `rank` (boundary psi owned by the sweeping rank): sizes[3] =
+ * {T3_local, n_send, n_recv}; then (each optional, NULL = skip) slot_first[S+1] (local first
+ * track of each stack), link[2 T3_local] (local target slot: < 2 T3_local owned, else the
+ * halo-send tail in peer blocks; -1 vacuum), recv_slots[n_recv] (local slots of received
+ * psi, peer-major), send_counts[world], recv_counts[world].  Call once with NULL arrays
+ * to size them. */
+int moc_rank_layout(const moc_problem* p, int32_t world, const int32_t* owner, int32_t rank, int64_t* sizes,
+                    int64_t* slot_first, int64_t* link, int64_t* recv_slots, int64_t* send_counts,
+                    int64_t* recv_counts);
 
 /* ---------------------------------------------------------------- solver */
 /* Multi-GPU: one process per GPU, `world` ranks.  Each rank sweeps its

@@ -136,6 +136,7 @@ SIGNATURES = {
     "moc_attenuation_probe": (C.c_int, [C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "moc_sweep_checksums": (C.c_int, [_vp, _vp, _vp]),
     "moc_iteration_sweep": (C.c_int, [_vp]),
+    "moc_rank_layout": (C.c_int, [_vp, C.c_int32, _vp, C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "moc_nccl_unique_id": (C.c_int, [_vp]),
     "moc_solver_set_exchange": (C.c_int, [_vp, EXCHANGE_FN, _vp]),
     "moc_iteration_finish": (C.c_int, [_vp]),
@@ -309,6 +310,19 @@ class Problem:
         out = np.zeros(n.value, np.int64)
         self._call(lib().moc_halo_plan, int(world), _p(own), int(rank), int(peer), _p(out), n.value, C.byref(n))
         return out
+
+    def rank_layout(self, world: int, owner, rank: int) -> dict:
+        """The solver's per-rank track numbering, local link table and halo layout."""
+        own = np.ascontiguousarray(owner, np.int32)
+        sz = np.zeros(3, np.int64)
+        L = lib()
+        self._call(L.moc_rank_layout, int(world), _p(own), int(rank), _p(sz), None, None, None, None, None)
+        S = self.stats()["n_stacks"]
+        sf, lk, rs = np.zeros(S + 1, np.int64), np.zeros(2 * sz[0], np.int64), np.zeros(sz[2], np.int64)
+        sc, rc = np.zeros(world, np.int64), np.zeros(world, np.int64)
+        self._call(L.moc_rank_layout, int(world), _p(own), int(rank), _p(sz), _p(sf), _p(lk), _p(rs), _p(sc), _p(rc))
+        return dict(T3_local=int(sz[0]), n_send=int(sz[1]), slot_first=sf, link=lk, recv_slots=rs, send_counts=sc,
+                    recv_counts=rc)
 
     def trace_track_3d(self, track: int, backward: bool = False):
         nseg = C.c_int64()

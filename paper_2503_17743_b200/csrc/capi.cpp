@@ -329,6 +329,30 @@ int moc_halo_plan(const moc_problem* p, int32_t world, const int32_t* owner, int
   })
 }
 
+int moc_rank_layout(const moc_problem* p, int32_t world, const int32_t* owner, int32_t rank, int64_t* sizes,
+                    int64_t* slot_first, int64_t* link, int64_t* recv_slots, int64_t* send_counts,
+                    int64_t* recv_counts) {
+  if (!p || !owner || !sizes || rank < 0 || rank >= world) return MOC_E_INVALID_ARG;
+  moc_problem* q = const_cast<moc_problem*>(p);
+  MOC_TRY(q, {
+    const Laydown& L = p->impl.lay;
+    if (!L.done) throw Error(MOC_E_STATE, "tracks not generated");
+    std::vector<int64_t> lk(2 * (size_t)L.n3);
+    links3d(p->impl.geo, L, lk.data());
+    std::vector<int32_t> own(owner, owner + L.S());
+    RankLayout rl;
+    rank_layout(L, lk.data(), own, rank, world, rl);
+    sizes[0] = rl.T3_local;
+    sizes[1] = rl.n_send;
+    sizes[2] = (int64_t)rl.recv_slots.size();
+    if (slot_first) std::copy(rl.slot_first.begin(), rl.slot_first.end(), slot_first);
+    if (link) std::copy(rl.link.begin(), rl.link.end(), link);
+    if (recv_slots) std::copy(rl.recv_slots.begin(), rl.recv_slots.end(), recv_slots);
+    if (send_counts) std::copy(rl.send_counts.begin(), rl.send_counts.end(), send_counts);
+    if (recv_counts) std::copy(rl.recv_counts.begin(), rl.recv_counts.end(), recv_counts);
+  })
+}
+
 // ---- Eq. 5: z_i(s) = z_0(0) + i dz + s cot(theta)
 double moc_z_of(double z0, double dz, int64_t i, double theta, double s) {
   return z0 + (double)i * dz + s * (std::cos(theta) / std::sin(theta));

@@ -113,6 +113,15 @@ void halo_plan(const Laydown& L, const int64_t* link, const std::vector<int32_t>
                std::vector<int64_t>& slots);
 void halo_plans(const Laydown& L, const int64_t* link, const std::vector<int32_t>& owner, int rank, int world,
                 std::vector<std::vector<int64_t>>& send, std::vector<std::vector<int64_t>>& recv);
+struct RankLayout {
+  int64_t T3_local = 0, n_send = 0;
+  std::vector<int64_t> slot_first;               // [S + 1] local first track of each stack
+  std::vector<int64_t> link;                     // [2 T3_local] local target slot (-1 vacuum)
+  std::vector<int64_t> recv_slots;               // local slots of received psi, peer-major
+  std::vector<int64_t> send_counts, recv_counts; // [world] slots per peer
+};
+void rank_layout(const Laydown& L, const int64_t* link, const std::vector<int32_t>& owner, int rank, int world,
+                 RankLayout& out);
 
 }  // namespace moc
 

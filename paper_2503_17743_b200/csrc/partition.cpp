@@ -89,6 +89,59 @@ void halo_plans(const Laydown& L, const int64_t* link, const std::vector<int32_t
     }
 }
 
+// This rank's track numbering and link table (boundary psi owned by the sweeping rank,
+// SURVEY §8(e)): its stacks' members in stack order get local ids 0..T3_local-1; a link to
+// an owned target becomes that target's local slot, a link to another rank's target the
+// next slot of that peer's block in the halo-send tail [2 T3_local, 2 T3_local + n_send)
+// (source-slot order, the order of halo_plans and of the peer's receive list); received
+// psi is scattered into recv_slots (local slots, peer-major).
+void rank_layout(const Laydown& L, const int64_t* link, const std::vector<int32_t>& owner, int rank, int world,
+                 RankLayout& out) {
+  const int64_t S = L.S();
+  out.slot_first.assign(S + 1, 0);
+  int64_t run = 0;
+  for (int64_t q = 0; q < S; ++q) {
+    out.slot_first[q] = run;
+    if (owner[q] == rank) run += L.st_cnt[q];
+  }
+  out.slot_first[S] = run;
+  out.T3_local = run;
+  auto stack_of = [&](int64_t gid) {
+    return (int64_t)(std::upper_bound(L.st_first.begin(), L.st_first.end(), gid) - L.st_first.begin() - 1);
+  };
+  auto local_slot = [&](int64_t gslot) {
+    const int64_t gid = gslot / 2, ts = stack_of(gid);
+    return 2 * (out.slot_first[ts] + (gid - L.st_first[ts])) + (gslot & 1);
+  };
+  std::vector<std::vector<int64_t>> send, recv;
+  halo_plans(L, link, owner, rank, world, send, recv);
+  std::vector<int64_t> soff(world + 1, 0);
+  out.send_counts.assign(world, 0);
+  out.recv_counts.assign(world, 0);
+  for (int p = 0; p < world; ++p) {
+    out.send_counts[p] = (int64_t)send[p].size();
+    out.recv_counts[p] = (int64_t)recv[p].size();
+    soff[p + 1] = soff[p] + out.send_counts[p];
+  }
+  out.n_send = soff[world];
+  out.link.assign(2 * out.T3_local, -1);
+  std::vector<int64_t> cnt(world, 0);
+  for (int64_t q = 0; q < S; ++q) {
+    if (owner[q] != rank) continue;
+    for (int64_t gid = L.st_first[q]; gid < L.st_first[q + 1]; ++gid)
+      for (int d = 0; d < 2; ++d) {
+        const int64_t tgt = link[2 * gid + d];
+        if (tgt < 0) continue;
+        const int rt = owner[stack_of(tgt / 2)];
+        out.link[2 * (out.slot_first[q] + (gid - L.st_first[q])) + d] =
+            rt == rank ? local_slot(tgt) : 2 * out.T3_local + soff[rt] + cnt[rt]++;
+      }
+  }
+  out.recv_slots.clear();
+  for (int p = 0; p < world; ++p)
+    for (int64_t x : recv[p]) out.recv_slots.push_back(local_slot(x));
+}
+
 void halo_plan(const Laydown& L, const int64_t* link, const std::vector<int32_t>& owner, int rank, int peer,
                std::vector<int64_t>& slots) {
   int world = 1 + std::max(rank, peer);

@@ -1250,61 +1250,26 @@ int moc_solver_create(moc_solver** out, moc_problem* p, int device, void* cuda_s
         std::vector<double> cost;
         partition_stacks(L, s->comm.world, owner, &cost);
         s->owned_cost = cost[s->comm.rank];
-        const int rank = s->comm.rank, W = s->comm.world;
-        // this rank's track numbering: its stacks' members, in stack order (boundary psi is
-        // owned by the rank that sweeps the track)
-        std::vector<int64_t> loc(s->S + 1);
-        int64_t run = 0;
-        for (int64_t q = 0; q < s->S; ++q) {
-          loc[q] = run;
-          if (owner[q] == rank) run += L.st_cnt[q];
-        }
-        loc[s->S] = run;
-        s->T3_local = run;
-        auto stack_of = [&](int64_t gid) {
-          return (int64_t)(std::upper_bound(L.st_first.begin(), L.st_first.end(), gid) - L.st_first.begin() - 1);
-        };
-        auto local_slot = [&](int64_t gslot) {
-          const int64_t gid = gslot / 2, ts = stack_of(gid);
-          return 2 * (loc[ts] + (gid - L.st_first[ts])) + (gslot & 1);
-        };
-        std::vector<std::vector<int64_t>> send, recv;
-        halo_plans(L, lk.data(), owner, rank, W, send, recv);
-        std::vector<int64_t> soff(W + 1, 0);
-        for (int p = 0; p < W; ++p) {
-          s->send_counts.push_back((int64_t)send[p].size());
-          s->recv_counts.push_back((int64_t)recv[p].size());
-          soff[p + 1] = soff[p] + (int64_t)send[p].size();
-        }
-        s->n_send = soff[W];
+        const int W = s->comm.world;
+        RankLayout rl;
+        rank_layout(L, lk.data(), owner, s->comm.rank, W, rl);
+        s->T3_local = rl.T3_local;
+        s->n_send = rl.n_send;
         s->psi_slots = 2 * s->T3_local + s->n_send;
-        // links in local slots: an owned target -> its local slot; another rank's target ->
-        // the next slot of the halo-send tail of its peer (source-slot order, the order of
-        // halo_plans and of the peer's receive list)
-        std::vector<uint32_t> l32(2 * s->T3_local, 0xffffffffu);
-        std::vector<int64_t> cnt(W, 0);
-        for (int64_t q = 0; q < s->S; ++q) {
-          if (owner[q] != rank) continue;
-          for (int64_t gid = L.st_first[q]; gid < L.st_first[q + 1]; ++gid)
-            for (int dd = 0; dd < 2; ++dd) {
-              const int64_t tgt = lk[2 * gid + dd];
-              const int64_t src = 2 * (loc[q] + (gid - L.st_first[q])) + dd;
-              if (tgt < 0) continue;
-              const int rt = owner[stack_of(tgt / 2)];
-              l32[src] = (uint32_t)(rt == rank ? local_slot(tgt) : 2 * s->T3_local + soff[rt] + cnt[rt]++);
-            }
-        }
+        s->send_counts = rl.send_counts;
+        s->recv_counts = rl.recv_counts;
+        std::vector<uint32_t> l32(rl.link.size());
+        for (size_t q = 0; q < l32.size(); ++q) l32[q] = rl.link[q] < 0 ? 0xffffffffu : (uint32_t)rl.link[q];
         s->d_link = dmalloc<uint32_t>(l32.size(), B);
         upload(l32.data(), s->d_link, 4 * l32.size(), st);
         std::vector<uint32_t> sf32(s->S + 1);
-        for (int64_t q = 0; q <= s->S; ++q) sf32[q] = (uint32_t)loc[q];
+        for (int64_t q = 0; q <= s->S; ++q) sf32[q] = (uint32_t)rl.slot_first[q];
         s->d_slot_first = dmalloc<uint32_t>(s->S + 1, B);
         upload(sf32.data(), s->d_slot_first, 4 * (s->S + 1), st);
         // halo: the send buffer is gathered from the tail; received psi scatter to local slots
-        std::vector<uint32_t> ss(s->n_send), rr;
+        std::vector<uint32_t> ss(s->n_send), rr(rl.recv_slots.size());
         for (int64_t x = 0; x < s->n_send; ++x) ss[x] = (uint32_t)(2 * s->T3_local + x);
-        for (int p = 0; p < W; ++p)
-          for (int64_t x : recv[p]) rr.push_back((uint32_t)local_slot(x));
+        for (size_t x = 0; x < rr.size(); ++x) rr[x] = (uint32_t)rl.recv_slots[x];
         s->n_recv = (int64_t)rr.size();
         s->d_send_slots = dmalloc<uint32_t>(ss.size(), B);
         s->d_recv_slots = dmalloc<uint32_t>(rr.size(), B);

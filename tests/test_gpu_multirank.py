@@ -128,6 +128,7 @@ def test_nccl_path_single_rank():
     kb, _ = b.iterate(6)
     assert kb == pytest.approx(ka, abs=1e-7)
     pa, pb = a.scalar_flux(), b.scalar_flux()
-    assert np.abs(pa - pb).max() / pa.max() < 1e-6
+    # equal up to the order of the fp32 tally reductions (global float atomics, run to run)
+    assert np.abs(pa - pb).max() / pa.max() < 1e-5
     rb = b.solve(tol_k=1e-7, tol_src=1e-6, max_iter=3000)
     assert rb["converged"]

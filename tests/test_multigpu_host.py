@@ -104,6 +104,65 @@ def test_halo_exchange_gloo(M, world):
     assert all(h > 0 for _, _, h, _ in res)
 
 
+def _worker_local(rank, world, port, prob, result_q):
+    """The solver's own per-rank layout (moc_rank_layout): local buffers of 2 T3_local +
+    n_send slots, local link writes, the halo-send tail sent per peer, received psi
+    scattered to local slots -- every owned slot must then hold what the serial Jacobi
+    hand-off over global slots puts there."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2503_17743_b200 as mod
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pr = mod.Problem(prob)
+    owner, _ = pr.partition(world)
+    lay = pr.rank_layout(world, owner, rank)
+    link = pr.links3d()
+    st = pr.stacks()
+    # global id of every local track (stack order of this rank's stacks)
+    gids = np.concatenate([np.arange(st["first"][q], st["first"][q + 1]) for q in range(len(st["count"]))
+                           if owner[q] == rank] or [np.zeros(0, np.int64)])
+    T3l = lay["T3_local"]
+    assert len(gids) == T3l and lay["slot_first"][-1] == T3l
+    buf = np.zeros(2 * T3l + lay["n_send"])
+    for ls in range(2 * T3l):  # outgoing value = global source slot + 1
+        if lay["link"][ls] >= 0:
+            buf[lay["link"][ls]] = 2 * gids[ls // 2] + (ls & 1) + 1.0
+    send_vals = torch.tensor(buf[2 * T3l:])
+    recv_vals = torch.zeros(int(lay["recv_counts"].sum()), dtype=torch.float64)
+    dist.all_to_all_single(recv_vals, send_vals, lay["recv_counts"].tolist(), lay["send_counts"].tolist())
+    buf[lay["recv_slots"]] = recv_vals.numpy()
+    src = np.zeros(len(link))
+    valid = link >= 0
+    src[link[valid]] = np.nonzero(valid)[0] + 1.0
+    gslots = (2 * gids[:, None] + np.arange(2)[None, :]).reshape(-1)
+    ok = np.array_equal(buf[:2 * T3l], src[gslots])
+    dist.barrier()
+    dist.destroy_process_group()
+    result_q.put((rank, ok, T3l, lay["n_send"]))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rank_local_layout_exchange_gloo(M, world):
+    import torch.multiprocessing as mp
+    prob = P.with_bc(P.small_lattice(3, 3, 3, quad=dict(num_azim=8, num_polar=4, radial_spacing=0.25,
+                                                          axial_spacing=0.5)), [1, 1, 1, 0, 1, 0])
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_local, args=(r, world, port, prob, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _, _ in res), res
+    assert sum(t for _, _, t, _ in res) == M.Problem(prob).stats()["n_tracks3d"]
+    assert all(n > 0 for _, _, _, n in res)
+
+
 # ---------------------------------------------------------------- NEA C5G7 table loader
 def test_xs_table_round_trip_and_validation(tmp_path):
     """problems.load_xs_table (SURVEY §8(f) unranked: real C5G7 data from a user file):
