@@ -49,7 +49,10 @@
 
 namespace {
 
-constexpr int kScWarps = 4;                  // independent warps (units) per CTA
+#ifndef MOC_SC_WARPS
+#define MOC_SC_WARPS 4
+#endif
+constexpr int kScWarps = MOC_SC_WARPS;       // independent warps (units) per CTA
 constexpr int kScThreads = 32 * kScWarps;
 #ifndef MOC_SC_CTAS_PER_SM
 #define MOC_SC_CTAS_PER_SM 3
