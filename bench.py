@@ -122,6 +122,41 @@ def _cpu_model():
     return None
 
 
+def _host_info():
+    """CPU record for the oracle leg: model, sockets, physical cores,
+    logical CPUs, RAM, OMP_NUM_THREADS."""
+    info = {"cpu_model": _cpu_model(), "logical_cpus": os.cpu_count(),
+            "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
+    try:
+        phys, sockets = set(), set()
+        cur = {}
+        for line in open("/proc/cpuinfo"):
+            if ":" in line:
+                k, v = [x.strip() for x in line.split(":", 1)]
+                cur[k] = v
+            elif cur:
+                sockets.add(cur.get("physical id"))
+                phys.add((cur.get("physical id"), cur.get("core id")))
+                cur = {}
+        info["sockets"] = len(sockets - {None}) or None
+        info["physical_cores"] = len({p for p in phys if p[1] is not None}) or None
+    except OSError:
+        pass
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                info["ram_gb"] = round(int(line.split()[1]) / 1048576, 1)
+    except OSError:
+        pass
+    return info
+
+
+PAPER_CONTEXT = ("PAPER.md:4 reports a 300-400x speedup of its GPU OTF/EXP MOC over 'traditional methods', "
+                 "and P:301 30-100x over OpenMOC, on a 12700KF / 32-core AMD host with 1080Ti, 2080Ti, 3060, "
+                 "4090 and MI60 GPUs (Table 1, P:250-260), precision unstated: context only, different "
+                 "hardware, problems and baselines")
+
+
 def oracle_sample(prob, target_s: float = 15.0):
     """Time the oracle as it stands on a bounded sample of the workload's tracks:
     every `stride`-th 3D track, swept once in both directions (re-traced explicitly)."""
@@ -135,7 +170,7 @@ def oracle_sample(prob, target_s: float = 15.0):
         stride = max(1, int(stride * sec / target_s))
     sec, nint = o.time_sample_sweep(stride)
     threads = oracle.num_threads()
-    return dict(value=nint / sec, unit=UNIT, cores=threads, kind="oracle", cpu_model=_cpu_model(),
+    return dict(value=nint / sec, unit=UNIT, cores=threads, kind="oracle", cpu_model=_cpu_model(), host=_host_info(),
                 sample=f"every {stride}th of {n3} 3D tracks ({(n3 + stride - 1) // stride} tracks, "
                        f"{nint:.3e} integrations, fp64, explicit re-trace + sweep, {sec:.1f} s on {threads} threads)",
                 seconds=sec, integrations=nint)
@@ -180,7 +215,8 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded C5G7-shaped XS, problems/)",
         "config": {"workload": WORKLOADS.get(args.config, f"cfg{args.config}"), "sample": base["sample"]},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": base["cores"], "kind": "oracle",
-                         "sample": base["sample"], "cpu_model": base.get("cpu_model")},
+                         "sample": base["sample"], "cpu_model": base.get("cpu_model"), "host": base.get("host")},
+        "paper_context": PAPER_CONTEXT,
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -320,7 +356,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = oracle_sample(prob, target_s=args.ref_seconds)
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "host")}
     # the unit that binds in practice (from the committed ncu --set full capture of this
     # kernel and config): the L1 LSU data pipe and the issue rate, next to R_ALU
     binding = None
@@ -367,6 +403,7 @@ def run_ours(args):
         "clocks": clocks,
         "cpu_baseline": cpu,
         "k_eff_err": kerr,
+        "paper_context": PAPER_CONTEXT,
         "sweep_s_per_iter": sweep_med * 1e-3,
     }
     if rank == 0:
