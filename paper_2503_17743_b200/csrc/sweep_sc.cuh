@@ -463,11 +463,35 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
       cell.hh = hh;
       cell.hc = hc;
       cell.nem = 0;
+#ifndef MOC_SC_NO_COLPF
+#define MOC_SC_COLPF 1
+#endif
+#ifdef MOC_SC_COLPF
+      // column data prefetched 32 columns at a time (lane i holds column kk0 + i: its 2D
+      // segment's two ends and region, one coalesced load each) and broadcast by shuffles
+      double pf_sa = 0.0, pf_sb = 0.0;
+      uint32_t pf_rg = 0;
+#endif
 #pragma unroll 1
       for (int kk = 0; kk < nk; ++kk) {
         const int k = ms ? nk - 1 - kk : kk;
+#ifdef MOC_SC_COLPF
+        if ((kk & 31) == 0) {
+          const int kq = kk + lane;
+          if (kq < nk) {
+            const int kx = ms ? nk - 1 - kq : kq;
+            pf_sa = kx ? d.seg_send[sb + kx - 1] : 0.0;
+            pf_sb = d.seg_send[sb + kx];
+            pf_rg = d.seg_region[sb + kx];
+          }
+        }
+        const double s_a = __shfl_sync(0xffffffffu, pf_sa, kk & 31);
+        const double s_b = __shfl_sync(0xffffffffu, pf_sb, kk & 31);
+        const uint32_t region_pf = __shfl_sync(0xffffffffu, pf_rg, kk & 31);
+#else
         const double s_a = k ? d.seg_send[sb + k - 1] : 0.0;
         const double s_b = d.seg_send[sb + k];
+#endif
         const double S = kk == 0 ? 0.0 : (ms ? Lt - s_b : s_a);
         const double w = s_b - s_a;
         const double base = zc0 + S * c, rho = w * c;
@@ -489,7 +513,11 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
           const int v = __double2int_ru((x - base) * invD);
           return min(max(v, 0), B);
         };
+#ifdef MOC_SC_COLPF
+        const uint32_t region = region_pf;
+#else
         const uint32_t region = d.seg_region[sb + k];
+#endif
         const float Lf = (float)(w * isn);
 #pragma unroll
         for (int g = 0; g < 8; ++g) cell.T[g] = 0.f;
