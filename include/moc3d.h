@@ -119,6 +119,13 @@ int moc_get_polar(const moc_problem* p, double* theta, double* dz, double* weigh
 /* 3D link table by index arithmetic: link[slot] = target slot or -1. */
 int moc_get_links3d(const moc_problem* p, int64_t* link);
 
+/* FSR volumes [J] on the problem (SURVEY §8(b) moc_get_fsr_volumes; host computation, no
+ * GPU): vol_track = the track estimate V_j = sum_{a,n} W_{a,n}/(2 pi) A_perp sum L from the
+ * host OTF walk over every 3D track (App. A.5), vol_analytic = area x layer height
+ * (S:83-85).  Either pointer may be NULL (not both).  The solver's moc_get_fsr_volumes
+ * returns the same track estimate from the device walk. */
+int moc_problem_fsr_volumes(const moc_problem* p, double* vol_track, double* vol_analytic);
+
 /* OTF 3D segments of one track (S:231 trace_segments_otf; Eqs. 5, 8, 11) computed on
  * the host with the same walk the device kernel runs.  Returns #segments in *nseg;
  * if cap < *nseg nothing is written and MOC_E_INVALID_ARG is returned. */

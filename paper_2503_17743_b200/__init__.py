@@ -137,6 +137,7 @@ SIGNATURES = {
     "moc_sweep_checksums": (C.c_int, [_vp, _vp, _vp]),
     "moc_iteration_sweep": (C.c_int, [_vp]),
     "moc_rank_layout": (C.c_int, [_vp, C.c_int32, _vp, C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "moc_problem_fsr_volumes": (C.c_int, [_vp, _vp, _vp]),
     "moc_nccl_unique_id": (C.c_int, [_vp]),
     "moc_solver_set_exchange": (C.c_int, [_vp, EXCHANGE_FN, _vp]),
     "moc_iteration_finish": (C.c_int, [_vp]),
@@ -310,6 +311,13 @@ class Problem:
         out = np.zeros(n.value, np.int64)
         self._call(lib().moc_halo_plan, int(world), _p(own), int(rank), int(peer), _p(out), n.value, C.byref(n))
         return out
+
+    def fsr_volumes(self):
+        """(track-estimated, analytic) FSR volumes [J] from the host walk (no GPU)."""
+        J = self.num_fsrs()
+        vt, va = np.zeros(J), np.zeros(J)
+        self._call(lib().moc_problem_fsr_volumes, _p(vt), _p(va))
+        return vt, va
 
     def rank_layout(self, world: int, owner, rank: int) -> dict:
         """The solver's per-rank track numbering, local link table and halo layout."""

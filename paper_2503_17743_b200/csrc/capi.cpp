@@ -7,6 +7,8 @@
 #include <cstring>
 #include <numeric>
 
+#include <omp.h>
+
 #include "host.h"
 
 using namespace moc;
@@ -276,6 +278,45 @@ int moc_trace_track_3d(const moc_problem* p, int64_t track3d, int64_t* fsr, doub
     ++q;
   });
   return MOC_OK;
+}
+
+// SURVEY §8(b) moc_get_fsr_volumes on the problem handle: track-estimated volumes from the
+// host OTF walk over every 3D track (App. A.5: V_j = sum W/(2 pi) A_perp L), OpenMP with
+// per-thread sums merged in thread order; analytic volumes S:83-85.
+static void host_track_volumes(const Geometry& g, const Laydown& L, double* vol) {
+  const int64_t J = g.n_fsr;
+  const OtfView v = otf_view_host(g, L);
+  const int nth = omp_get_max_threads();
+  std::vector<std::vector<double>> part(nth, std::vector<double>((size_t)J, 0.0));
+#pragma omp parallel num_threads(nth)
+  {
+    std::vector<double>& V = part[omp_get_thread_num()];
+#pragma omp for schedule(static)
+    for (int64_t s = 0; s < L.S(); ++s) {
+      const int64_t t = s / L.N;
+      const size_t an = (size_t)L.t_a[t] * L.N + (size_t)(s % L.N);
+      const double w = L.an_w[an] / (2.0 * 3.14159265358979323846) * L.an_aperp[an];
+      for (int64_t id = L.st_first[s]; id < L.st_first[s + 1]; ++id) {
+        const TrackGeo tg = track_geo(g, L, id, nullptr);
+        otf_walk_fwd(v, tg, [&](int64_t k, int ly, double len) { V[(size_t)(v.seg_region[k] * v.NL + ly)] += w * len; });
+      }
+    }
+  }
+  for (int64_t j = 0; j < J; ++j) {
+    double a = 0.0;
+    for (int th = 0; th < nth; ++th) a += part[th][j];
+    vol[j] = a;
+  }
+}
+
+int moc_problem_fsr_volumes(const moc_problem* p, double* vol_track, double* vol_analytic) {
+  if (!p || (!vol_track && !vol_analytic)) return MOC_E_INVALID_ARG;
+  moc_problem* q = const_cast<moc_problem*>(p);
+  MOC_TRY(q, {
+    if (!p->impl.lay.done) throw Error(MOC_E_STATE, "tracks not generated");
+    if (vol_analytic) p->impl.geo.analytic_volumes(vol_analytic);
+    if (vol_track) host_track_volumes(p->impl.geo, p->impl.lay, vol_track);
+  })
 }
 
 /* host-side backward walk (test hook: the backward list must mirror the forward one) */

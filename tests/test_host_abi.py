@@ -224,3 +224,17 @@ def test_raw_segment_estimate_bounds_exact_count(M, oracle_mod):
     pr = M.Problem(prob)
     tot = oracle_mod.Oracle(prob).total_segments3d()
     assert pr.stats()["n_segs3d_raw"] >= tot
+
+
+def test_problem_fsr_volumes_match_oracle(M, oracle_mod):
+    """SURVEY §8(b) moc_get_fsr_volumes on the problem handle (host walk): track-estimated
+    volumes equal the oracle's (its own brute-force tracer) and the analytic ones equal
+    area x height; the per-FSR track estimate is within 2 % of analytic
+    and the total is exact (P9)."""
+    prob = P.config(2)
+    vt, va = M.Problem(prob).fsr_volumes()
+    ot, oa = oracle_mod.Oracle(prob).volumes()
+    np.testing.assert_allclose(vt, ot, rtol=1e-10)
+    np.testing.assert_allclose(va, oa, rtol=1e-12)
+    assert np.max(np.abs(vt - va) / va) < 0.02
+    assert vt.sum() == pytest.approx(1.26 * 1.26 * 10.0, rel=1e-12)
