@@ -622,8 +622,10 @@ void upload(const void* h, void* d, size_t bytes, cudaStream_t st) {
 // The __constant__ tables (cross sections, axial planes) are per device, shared by every
 // solver in the process: the solver whose kernels run next re-uploads its own copies when it
 // is not the last owner (one solver active per device at a time; stream-ordered uploads).
-uint64_t& const_owner(int dev) {
-  static uint64_t owner[64] = {};
+// (atomic: several host threads may each drive their own solver; the tables themselves are
+// still one set per device, so solvers sharing a device must not run concurrently)
+std::atomic<uint64_t>& const_owner(int dev) {
+  static std::atomic<uint64_t> owner[64] = {};
   return owner[dev & 63];
 }
 void ensure_constants(moc_solver* s) {
