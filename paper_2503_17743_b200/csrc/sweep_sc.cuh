@@ -418,11 +418,14 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
     const double c = fabs(cot), invD = 1.0 / dz;
     const float ti = (float)(isn * fabs(tn));  // 3D length per unit of z: 1/|cos(theta)|
     const float dzf = (float)dz;
-    const int B = (int)U.n, lgR = (int)U.lgR, R = 1 << lgR, C = 32 >> lgR;
+    const int B = (int)U.n, lgRu = (int)U.lgR;
+    // largest R for a column: keep >= 3 members of a full cell per lane (hmin / dz members
+    // per cell), below which the per-lane cell setup outweighs the split member work
+    int lgRcap = lgRu;
+    while (lgRcap < 3 && a.inv_hmin * (double)(6 << lgRcap) * dz <= 1.0) ++lgRcap;
     const bool up = cot > 0;
     const uint32_t id0 = a.slot_first[s] + U.i0;  // this rank's track numbering (psi, links)
     const float cw = d.an_c[an];
-    const int ci = lane >> lgR, r = lane & (R - 1);
 
     for (int dir = 0; dir < 2; ++dir) {
       const bool ms = dir == 1;
@@ -501,6 +504,13 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
         while (L_lo < NL - 1 && P[L_lo + 1] <= base) ++L_lo;
         if (L_hi < L_lo) L_hi = L_lo;
         while (L_hi < NL - 1 && P[L_hi + 1] < top) ++L_hi;
+        // lanes per cell for this column: the unit's R, raised while the column's cells
+        // still fit (a band entering or leaving the domain touches few layers: its members
+        // are then split over R = 2, 4, 8 lanes per cell instead of idling lanes)
+        int lgR = lgRu;
+        while (lgR < lgRcap && (32 >> (lgR + 1)) >= L_hi - L_lo + 1) ++lgR;
+        const int R = 1 << lgR, C = 32 >> lgR;
+        const int ci = lane >> lgR, r = lane & (R - 1);
         int Lh = L_hi;
         if (Lh - L_lo + 1 > C) {
           if (lane == 0) atomicAdd(a.err, 1);
