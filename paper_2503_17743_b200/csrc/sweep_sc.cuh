@@ -458,6 +458,10 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
       // band layer window [L_lo, L_hi]: both ends only rise along the canonical walk
       // (base and top = base of the next column + (B - 1) dz are non-decreasing)
       int L_lo = 0, L_hi = 0;
+      // P[L_lo + 1] and P[L_hi + 1] kept in registers (+inf above the top layer): the
+      // window ends move in few columns, so the common case needs no shared-memory load
+      const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+      double PnLo = NL > 1 ? P[1] : kInf, PnHi = PnLo;
       if (lane == 0) SC_STAT(0, 1);
       __syncwarp();
       ScCell<G, GP, HASH> cell;
@@ -501,9 +505,18 @@ __global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a)
         if (base >= d.Z) break;  // every member of the band has left through the top
         const double top = base + (double)(B - 1) * dz + rho;
         if (top <= 0.0) continue;  // no member has entered yet
-        while (L_lo < NL - 1 && P[L_lo + 1] <= base) ++L_lo;
-        if (L_hi < L_lo) L_hi = L_lo;
-        while (L_hi < NL - 1 && P[L_hi + 1] < top) ++L_hi;
+        while (PnLo <= base) {
+          ++L_lo;
+          PnLo = L_lo < NL - 1 ? P[L_lo + 1] : kInf;
+        }
+        if (L_hi < L_lo) {
+          L_hi = L_lo;
+          PnHi = PnLo;
+        }
+        while (PnHi < top) {
+          ++L_hi;
+          PnHi = L_hi < NL - 1 ? P[L_hi + 1] : kInf;
+        }
         // lanes per cell for this column: the unit's R, raised while the column's cells
         // still fit (a band entering or leaving the domain touches few layers: its members
         // are then split over R = 2, 4, 8 lanes per cell instead of idling lanes)
