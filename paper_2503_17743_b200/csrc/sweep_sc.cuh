@@ -201,6 +201,33 @@ struct ScCell {
     return n;
   }
 
+  // visit() one member per trip: a single inlined copy of the member body (the per-member
+  // exponential classes carry enough independent work per member; the sweep's hot code
+  // must stay inside the 32 KB instruction cache)
+  template <int STAT_TRIP, int STAT_CALL, class F1>
+  __device__ __forceinline__ int visit1(int a, int b, int r, int lgR, int c, F1&& f1) {
+    const int R = 1 << lgR;
+    const int a1 = a + ((r - a) & (R - 1));
+    if (a1 >= b) return 0;
+    const int n = ((b - 1 - a1) >> lgR) + 1;
+    int idx = ((((c << lgR) + r - a1) & 7) >> lgR);
+    if (idx >= n) idx = 0;
+#pragma unroll 1
+    for (int left = n; left > 0; --left) {
+      f1(a1 + (idx << lgR));
+      ++idx;
+      idx = idx == n ? 0 : idx;
+    }
+#ifdef MOC_SC_STATS
+    {
+      const unsigned am = __activemask();
+      const int mx = __reduce_max_sync(am, (unsigned)n);
+      if ((threadIdx.x & 31) == __ffs(am) - 1) SC_STAT(STAT_TRIP, mx), SC_STAT(STAT_CALL, 1);
+    }
+#endif
+    return n;
+  }
+
   // shared-E class (Eq. 8 / Eq. 11 pieces of one cell, all of length L):
   // psi' = psi E + q (1 - E); T += (sum psi - n q)(1 - E)
   __device__ __forceinline__ void full(int a, int b, int r, int lgR, int c, float L) {
@@ -254,29 +281,8 @@ struct ScCell {
   __device__ __forceinline__ void corner(int a, int b, int r, int lgR, int c, int anchor, float d0, float dzf,
                                          float ti) {
     if (a >= b) return;
-    const int n = visit<7, 9>(
+    const int n = visit1<7, 9>(
         a, b, r, lgR, c,
-        [&](int m0, int m1) {
-          const float L0 = fmaf((float)abs(m0 - anchor), dzf, d0) * ti;
-          const float L1 = fmaf((float)abs(m1 - anchor), dzf, d0) * ti;
-          float v0[4 * NH], v1[4 * NH];
-          load(m0, v0);
-          load(m1, v1);
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const float E0 = ex2_approx(-sg[g] * L0), E1 = ex2_approx(-sg[g] * L1);
-            const float d0_ = v0[g] - q[g], d1_ = v1[g] - q[g];
-            const float l0 = fmaf(-d0_, E0, d0_), l1 = fmaf(-d1_, E1, d1_);
-            v0[g] -= l0;
-            v1[g] -= l1;
-            T[g] += l0;
-            T[g] += l1;
-          }
-          store(m0, v0);
-          store(m1, v1);
-          emit_hash(m0);
-          emit_hash(m1);
-        },
         [&](int m) {
           const float L = fmaf((float)abs(m - anchor), dzf, d0) * ti;
           float v[4 * NH];
@@ -342,19 +348,8 @@ struct ScCell {
         }
       }
     };
-    const int n = visit<7, 9>(
+    const int n = visit1<7, 9>(
         a, b, r, lgR, c,
-        [&](int m0, int m1) {
-          float v0[4 * NH], v1[4 * NH];
-          load(m0, v0);
-          load(m1, v1);
-          one(m0, v0);
-          one(m1, v1);
-          store(m0, v0);
-          store(m1, v1);
-          emit(m0);
-          emit(m1);
-        },
         [&](int m) {
           float v[4 * NH];
           load(m, v);
