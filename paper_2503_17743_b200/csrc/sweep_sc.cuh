@@ -170,42 +170,13 @@ struct ScCell {
   }
 
   // members m = a1, a1 + R, ... < b (all = r mod R) in a bank-rotated order (the lanes of
-  // a quarter-warp start on distinct 16-byte bank groups: member m -> group m mod 8), two
-  // members per trip (independent load -> update -> store chains); returns the count
-  template <int STAT_TRIP, int STAT_CALL, class F2, class F1>
-  __device__ __forceinline__ int visit(int a, int b, int r, int lgR, int c, F2&& f2, F1&& f1) {
-    const int R = 1 << lgR;
-    const int a1 = a + ((r - a) & (R - 1));
-    if (a1 >= b) return 0;
-    const int n = ((b - 1 - a1) >> lgR) + 1;
-    int idx = ((((c << lgR) + r - a1) & 7) >> lgR);
-    if (idx >= n) idx = 0;
-    int left = n;
-#pragma unroll 1
-    while (left >= 2) {
-      int i1 = idx + 1;
-      i1 = i1 == n ? 0 : i1;
-      f2(a1 + (idx << lgR), a1 + (i1 << lgR));
-      idx = i1 + 1;
-      idx = idx == n ? 0 : idx;
-      left -= 2;
-    }
-    if (left) f1(a1 + (idx << lgR));
-#ifdef MOC_SC_STATS
-    {
-      const unsigned am = __activemask();
-      const int mx = __reduce_max_sync(am, (unsigned)((n + 1) >> 1));
-      if ((threadIdx.x & 31) == __ffs(am) - 1) SC_STAT(STAT_TRIP, mx), SC_STAT(STAT_CALL, 1);
-    }
-#endif
-    return n;
-  }
-
-  // visit() one member per trip: a single inlined copy of the member body (the per-member
-  // exponential classes carry enough independent work per member; the sweep's hot code
-  // must stay inside the 32 KB instruction cache)
+  // a quarter-warp start on distinct 16-byte bank groups: member m -> group m mod 8), one
+  // member per trip: a single inlined copy of the member body, because the sweep's hot
+  // code must stay inside the 32 KB instruction cache (ncu: three copies per class put
+  // 99 % of the executed instructions in 30 KB and cost 6 % over this form; 46 KB cost
+  // 35 %); returns the count
   template <int STAT_TRIP, int STAT_CALL, class F1>
-  __device__ __forceinline__ int visit1(int a, int b, int r, int lgR, int c, F1&& f1) {
+  __device__ __forceinline__ int visit(int a, int b, int r, int lgR, int c, F1&& f1) {
     const int R = 1 << lgR;
     const int a1 = a + ((r - a) & (R - 1));
     if (a1 >= b) return 0;
@@ -242,22 +213,6 @@ struct ScCell {
     }
     const int n = visit<6, 8>(
         a, b, r, lgR, c,
-        [&](int m0, int m1) {
-          float v0[4 * NH], v1[4 * NH];
-          load(m0, v0);
-          load(m1, v1);
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            S[g] += v0[g];
-            S[g] += v1[g];
-            v0[g] = fmaf(v0[g], E[g], qc[g]);
-            v1[g] = fmaf(v1[g], E[g], qc[g]);
-          }
-          store(m0, v0);
-          store(m1, v1);
-          emit_hash(m0);
-          emit_hash(m1);
-        },
         [&](int m) {
           float v[4 * NH];
           load(m, v);
@@ -281,7 +236,7 @@ struct ScCell {
   __device__ __forceinline__ void corner(int a, int b, int r, int lgR, int c, int anchor, float d0, float dzf,
                                          float ti) {
     if (a >= b) return;
-    const int n = visit1<7, 9>(
+    const int n = visit<7, 9>(
         a, b, r, lgR, c,
         [&](int m) {
           const float L = fmaf((float)abs(m - anchor), dzf, d0) * ti;
@@ -348,7 +303,7 @@ struct ScCell {
         }
       }
     };
-    const int n = visit1<7, 9>(
+    const int n = visit<7, 9>(
         a, b, r, lgR, c,
         [&](int m) {
           float v[4 * NH];

@@ -37,7 +37,7 @@ for cfg in [int(x) for x in sys.argv[1:] if "=" not in x] or [4]:
     d["corner_frac"] = d["corner_pieces"] / (d["full_pieces"] + d["corner_pieces"])
     d["q_per_column"] = d["q_trips"] / d["columns"]
     d["columns_per_unit_dir"] = d["columns"] / d["unit_dirs"]
-    d["full_lane_eff"] = d["full_pieces"] / max(1, 64 * d["full_warp_trips"])
+    d["full_lane_eff"] = d["full_pieces"] / max(1, 32 * d["full_warp_trips"])  # one member per trip
     d["corner_lane_eff"] = d["corner_pieces"] / max(1, 2 * 32 * d["corner_warp_trips"])  # one member (two pieces) per trip
     print(json.dumps(d), flush=True)
     del s
