@@ -389,6 +389,7 @@ def run_ours(args):
                    "host_laydown_s": round(t_lay, 2), "device_setup_s": round(t_setup, 2),
                    "sweep_ms_median": sweep_med, "device_gb": round(tm["device_bytes"] / 1e9, 2),
                    "emitted_last": emitted, "emitted_expected": 2 * tm["n_segs3d"] if world == 1 else None,
+                   "sc_units_by_ctas_per_sm": dict(zip(("3", "4", "5"), tm.get("sc_units", [0, 0, 0]))),
                    "backend": backend if world > 1 else None, "per_rank_ms": rank_ms,
                    "cuda_graph": True},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT, "frac": achieved / peak,

@@ -217,8 +217,8 @@ typedef struct {
   int32_t exp_budget_mb;    /* EXP budget in MiB (0 = free device memory after allocation) */
   double exp_fraction;      /* fraction of the budget (0 = the paper's 0.8) */
   int32_t sc_lanes_per_cell; /* schedule 3: lanes per (2D segment, layer) cell, 1/2/4/8 (0 = per stack) */
-  int32_t sc_psi_cap;        /* schedule 3: boundary-psi band capacity per warp in members (0 = fill
-                                the shared memory of kScMinBlocks CTAs per SM) */
+  int32_t sc_psi_cap;        /* schedule 3: cap on the boundary-psi band capacity per warp in
+                                members (0 = fill the shared memory of the stack's CTAs per SM) */
   int32_t v2_lane_stride;    /* schedule 0: force the member stride between the lanes of a warp to
                                 1, 2, 4 or 8 (0 = per unit from the stack's dz; for tests) */
   int32_t no_graph;          /* 1: launch every iteration's kernels individually instead of
@@ -230,6 +230,10 @@ typedef struct {
                                 links) instead of last iteration's (Jacobi, Q9).  Halves the psi
                                 memory; the iterates differ (parity at convergence only), order
                                 and therefore results are not bitwise reproducible run to run */
+  int32_t sc_ctas_per_sm;    /* schedule 3: CTAs per SM of the sweep for every stack, 3, 4 or 5
+                                (else MOC_E_PARAM); 0 = per stack, the most CTAs per SM (more
+                                resident warps, smaller shared-memory psi bands) that do not cut
+                                the stack into more bands than 3 CTAs per SM do */
 } moc_solver_opts;
 
 /* Upload the laydown to `device`, allocate HBM state (boundary psi double buffer,
@@ -307,6 +311,8 @@ typedef struct {
   int64_t emitted_last;      /* merged segment-direction applications of Eq. 3-4 in the last
                                 iteration's sweep on this rank (integrity counter: equals
                                 2 * n_segs3d on one GPU); -1 if it could not be read */
+  int64_t sc_units[3];       /* schedule 3: work units swept at 3, 4 and 5 CTAs per SM (one
+                                sweep launch per non-empty group) */
 } moc_timings;
 int moc_get_timings(moc_solver* s, moc_timings* t);
 

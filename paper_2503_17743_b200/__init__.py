@@ -67,7 +67,7 @@ class moc_solver_opts(C.Structure):
                 ("deterministic", C.c_int32), ("tile_cells", C.c_int32), ("exp_mode", C.c_int32),
                 ("exp_budget_mb", C.c_int32), ("exp_fraction", C.c_double),
                 ("sc_lanes_per_cell", C.c_int32), ("sc_psi_cap", C.c_int32), ("v2_lane_stride", C.c_int32),
-                ("no_graph", C.c_int32), ("gauss_seidel", C.c_int32)]
+                ("no_graph", C.c_int32), ("gauss_seidel", C.c_int32), ("sc_ctas_per_sm", C.c_int32)]
 
 
 class moc_solve_opts(C.Structure):
@@ -83,7 +83,7 @@ class moc_timings(C.Structure):
     _fields_ = [("n_segs3d", C.c_int64), ("n_integrations", C.c_int64), ("sweep_ms_last", C.c_double),
                 ("iter_ms_last", C.c_double), ("launches_per_iter", C.c_int64), ("setup_ms", C.c_double),
                 ("device_bytes", C.c_int64), ("exp_segments", C.c_int64), ("exp_bytes", C.c_int64),
-                ("emitted_last", C.c_int64)]
+                ("emitted_last", C.c_int64), ("sc_units", C.c_int64 * 3)]
 
 
 class moc_comm_buffers(C.Structure):
@@ -358,7 +358,7 @@ class Solver:
                  blocks: int = 0, rank: int = 0, world: int = 1, tile_cells: int = 0, exp_mode: int = 0,
                  exp_budget_mb: int = 0, exp_fraction: float = 0.0, sc_lanes_per_cell: int = 0,
                  sc_psi_cap: int = 0, v2_lane_stride: int = 0, no_graph: bool = False, backend: str | None = None,
-                 gauss_seidel: bool = False):
+                 gauss_seidel: bool = False, sc_ctas_per_sm: int = 0):
         """world > 1: one rank of a torch.distributed job.  backend "nccl"
         (default when the process group is NCCL): the library owns an NCCL communicator
         and runs the whole iteration on the device; "gloo": the exchange is staged through
@@ -375,7 +375,7 @@ class Solver:
                 stream = 0
         opts = moc_solver_opts(schedule, threads, blocks, 0, tile_cells, exp_mode, exp_budget_mb, exp_fraction,
                                sc_lanes_per_cell, sc_psi_cap, v2_lane_stride, int(bool(no_graph)),
-                               int(bool(gauss_seidel)))
+                               int(bool(gauss_seidel)), sc_ctas_per_sm)
         comm = moc_comm_desc(rank, world, MOC_COMM_CALLER)
         if world == 1 and backend == "nccl":  # 1-rank communicator (tests the NCCL path on one GPU)
             comm.backend = MOC_COMM_NCCL
@@ -545,7 +545,8 @@ class Solver:
     def timings(self) -> dict:
         t = moc_timings()
         self._call(lib().moc_get_timings, C.byref(t))
-        return {f: getattr(t, f) for f, _ in moc_timings._fields_}
+        return {f: (list(getattr(t, f)) if isinstance(getattr(t, f), C.Array) else getattr(t, f))
+                for f, _ in moc_timings._fields_}
 
     def comm_buffers(self) -> dict:
         b = moc_comm_buffers()

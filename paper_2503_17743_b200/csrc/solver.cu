@@ -594,8 +594,15 @@ struct moc_solver {
   // stack-collective sweep (schedule 3, sweep_sc.cuh)
   ScUnit* d_sc_units = nullptr;
   uint32_t n_sc_units = 0;
-  size_t sc_smem = 0, sc_smem_hash = 0;
-  int sc_pcap = 0, sc_blocks = 0, sc_blocks_hash = 0;
+  // per occupancy g (kScMinBlocksList[g] CTAs per SM): psi band capacity, dynamic shared
+  // memory, grid, and the units it sweeps (d_sc_units[first, first + n))
+  struct ScGroup {
+    int pcap = 0, blocks = 0;
+    size_t smem = 0;
+    uint32_t first = 0, n = 0;
+  } sc_grp[3];
+  size_t sc_smem_hash = 0;
+  int sc_blocks_hash = 0;
   double hmin = 0;
   // multi-GPU (world > 1)
   uint32_t *d_send_slots = nullptr, *d_recv_slots = nullptr;
@@ -677,9 +684,6 @@ template <int G, int GP, bool HASH = false>
 void run_sweep_sc(moc_solver* s, unsigned long long* hash = nullptr, int32_t* nseg = nullptr) {
   ScArgs a;
   a.d = s->dd;
-  a.units = s->d_sc_units;
-  a.n_units = s->n_sc_units;
-  a.counter = s->d_counter;
   a.link = s->d_link;
   a.mat = s->d_mat;
   a.qt = s->d_qt;
@@ -688,7 +692,6 @@ void run_sweep_sc(moc_solver* s, unsigned long long* hash = nullptr, int32_t* ns
   a.psi_out = s->d_psi[1 - s->cur];
   a.tally = s->d_tally32;
   a.sc = s->d_sc;
-  a.pcap = s->sc_pcap;
   a.inv_hmin = (1.0 / s->hmin) * (1.0 + 1e-12);
   a.h_fast = s->hmin * (1.0 - 1e-9);
   a.err = s->d_err;
@@ -696,8 +699,26 @@ void run_sweep_sc(moc_solver* s, unsigned long long* hash = nullptr, int32_t* ns
   a.nseg = nseg;
   a.gs = s->opts.gauss_seidel;
   a.slot_first = s->d_slot_first ? s->d_slot_first : s->d_st_first;
-  k_sweep_sc<G, GP, HASH><<<HASH ? s->sc_blocks_hash : s->sc_blocks, kScThreads, HASH ? s->sc_smem_hash : s->sc_smem,
-                            s->stream>>>(a);
+  if constexpr (HASH) {  // every unit, 3 CTAs per SM (the largest band capacity)
+    a.units = s->d_sc_units;
+    a.n_units = s->n_sc_units;
+    a.counter = s->d_counter;
+    a.pcap = s->sc_grp[0].pcap;
+    k_sweep_sc<G, GP, true, 3><<<s->sc_blocks_hash, kScThreads, s->sc_smem_hash, s->stream>>>(a);
+  } else {
+    // one launch per occupancy group, each with its own unit queue counter
+    for (int g = 0; g < 3; ++g) {
+      const auto& q = s->sc_grp[g];
+      if (q.n == 0) continue;
+      a.units = s->d_sc_units + q.first;
+      a.n_units = q.n;
+      a.counter = s->d_counter + g;
+      a.pcap = q.pcap;
+      if (g == 0) k_sweep_sc<G, GP, false, 3><<<q.blocks, kScThreads, q.smem, s->stream>>>(a);
+      else if (g == 1) k_sweep_sc<G, GP, false, 4><<<q.blocks, kScThreads, q.smem, s->stream>>>(a);
+      else k_sweep_sc<G, GP, false, 5><<<q.blocks, kScThreads, q.smem, s->stream>>>(a);
+    }
+  }
 }
 
 template <int G, int GP>
@@ -799,7 +820,7 @@ void iter_sweep_half(moc_solver* s, bool time_it) {
   }
   if (f32t) {
     CUDA_OK(cudaMemsetAsync(s->d_tally32, 0, sizeof(float) * s->J * s->GP, s->stream));
-    CUDA_OK(cudaMemsetAsync(s->d_counter, 0, 2 * sizeof(uint32_t), s->stream));
+    CUDA_OK(cudaMemsetAsync(s->d_counter, 0, (s->opts.schedule == 3 ? 4 : 2) * sizeof(uint32_t), s->stream));
   } else {
     CUDA_OK(cudaMemsetAsync(s->d_tally, 0, sizeof(double) * s->J * s->GP, s->stream));
   }
@@ -918,31 +939,43 @@ iter_fn pick_iter(int G) {
   }
 }
 
-// schedule 3 (sweep_sc.cuh): shared memory per CTA = the warps' psi bands (+ hash state
-// for the checksum variant); kScMinBlocks CTAs per SM
-template <int G, int GP>
-void sc_smem_configure(moc_solver* s) {
+// schedule 3 (sweep_sc.cuh): shared memory per CTA = the warps' psi bands + cell staging,
+// for 3, 4 and 5 CTAs per SM (the checksum variant: 3 CTAs, + hash state per member)
+template <int G, int GP, int MINB>
+void sc_smem_configure_one(moc_solver* s, int g, int nsm) {
   cudaFuncAttributes fa{};
-  CUDA_OK(cudaFuncGetAttributes(&fa, k_sweep_sc<G, GP, false>));
-  const size_t per_cta = (228 * 1024) / kScMinBlocks - 1024 - fa.sharedSizeBytes;
+  CUDA_OK(cudaFuncGetAttributes(&fa, k_sweep_sc<G, GP, false, MINB>));
+  const size_t per_cta = (228 * 1024) / MINB - 1024 - fa.sharedSizeBytes;
   constexpr int NH = ScH<G>::NH;
   const size_t stage = (size_t)kScWarps * 32 * 64;  // per-warp cell staging (fast path)
-  int pcap = s->opts.sc_psi_cap > 0 ? s->opts.sc_psi_cap : (int)((per_cta - stage) / ((size_t)kScWarps * NH * 16));
+  int pcap = (int)((per_cta - stage) / ((size_t)kScWarps * NH * 16));
+  if (s->opts.sc_psi_cap > 0) pcap = std::min(pcap, s->opts.sc_psi_cap);
   pcap = std::max(32, pcap & ~31);
-  s->sc_pcap = pcap;
-  s->sc_smem = (size_t)kScWarps * NH * pcap * 16 + stage;
-  s->sc_smem_hash = s->sc_smem + (size_t)kScWarps * pcap * 12;
-  CUDA_OK(cudaFuncSetAttribute(k_sweep_sc<G, GP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->sc_smem));
-  CUDA_OK(cudaFuncSetAttribute(k_sweep_sc<G, GP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)s->sc_smem_hash));
-  int per_sm = 0, per_sm_h = 0, dev = 0, nsm = 0;
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_sc<G, GP, false>, kScThreads, s->sc_smem));
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_h, k_sweep_sc<G, GP, true>, kScThreads,
-                                                        s->sc_smem_hash));
-  if (per_sm < 1 || per_sm_h < 1) throw Error(MOC_E_CAPACITY, "stack-collective sweep does not fit on an SM");
+  auto& q = s->sc_grp[g];
+  q.pcap = pcap;
+  q.smem = (size_t)kScWarps * NH * pcap * 16 + stage;
+  CUDA_OK(cudaFuncSetAttribute(k_sweep_sc<G, GP, false, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q.smem));
+  int per_sm = 0;
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_sc<G, GP, false, MINB>, kScThreads, q.smem));
+  if (per_sm < 1) throw Error(MOC_E_CAPACITY, "stack-collective sweep does not fit on an SM");
+  q.blocks = nsm * per_sm;
+}
+
+template <int G, int GP>
+void sc_smem_configure(moc_solver* s) {
+  int dev = 0, nsm = 0;
   CUDA_OK(cudaGetDevice(&dev));
   CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  s->sc_blocks = nsm * per_sm;
+  sc_smem_configure_one<G, GP, 3>(s, 0, nsm);
+  sc_smem_configure_one<G, GP, 4>(s, 1, nsm);
+  sc_smem_configure_one<G, GP, 5>(s, 2, nsm);
+  s->sc_smem_hash = s->sc_grp[0].smem + (size_t)kScWarps * s->sc_grp[0].pcap * 12;
+  CUDA_OK(cudaFuncSetAttribute(k_sweep_sc<G, GP, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)s->sc_smem_hash));
+  int per_sm_h = 0;
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_h, k_sweep_sc<G, GP, true, 3>, kScThreads,
+                                                        s->sc_smem_hash));
+  if (per_sm_h < 1) throw Error(MOC_E_CAPACITY, "stack-collective sweep does not fit on an SM");
   s->sc_blocks_hash = nsm * per_sm_h;
 }
 
@@ -965,7 +998,10 @@ void sc_smem_configure_any(moc_solver* s) {
 // most floor(((B - 1) dz + rho_max) / h_min) + 2 layers: B is the largest band whose
 // cells fit C = 32 / R lanes' cells and whose psi fits the warp's share of shared memory;
 // R is the smallest for which a band fits at all (R = 1 unless a 2D segment rises through
-// more than 30 layers).  Units are sorted by exact segment count, descending.
+// more than 30 layers).  Each stack goes to the occupancy group with the most CTAs per SM
+// (3, 4, 5: more warps to hide latency, smaller psi bands) whose band capacity does not cut
+// it into more bands than 3 CTAs per SM do (opts.sc_ctas_per_sm forces one group).  Within
+// a group units are sorted by exact segment count, descending.
 void sc_configure(moc_solver* s, const Geometry& g, const Laydown& L, const std::vector<int32_t>& owner) {
   int64_t& Bytes = s->dev_bytes;
   cudaStream_t st = s->stream;
@@ -974,7 +1010,9 @@ void sc_configure(moc_solver* s, const Geometry& g, const Laydown& L, const std:
   for (int l = 0; l < g.NL; ++l) hmin = std::min(hmin, g.planes[l + 1] - g.planes[l]);
   s->hmin = hmin;
   if (g.NL + 1 > kMaxPlanes) throw Error(MOC_E_CAPACITY, "more than 255 axial layers");
-  std::vector<ScUnit> units;
+  std::vector<ScUnit> ug[3];
+  const int fctas = s->opts.sc_ctas_per_sm;
+  if (fctas != 0 && (fctas < 3 || fctas > 5)) throw Error(MOC_E_PARAM, "sc_ctas_per_sm must be 0, 3, 4 or 5");
   const int forced = s->opts.sc_lanes_per_cell;
   if (forced != 0 && forced != 1 && forced != 2 && forced != 4 && forced != 8)
     throw Error(MOC_E_PARAM, "sc_lanes_per_cell must be 0, 1, 2, 4 or 8");
@@ -991,25 +1029,41 @@ void sc_configure(moc_solver* s, const Geometry& g, const Laydown& L, const std:
     }
     const double D = L.an_dz[an], rho = wmax * std::fabs(L.an_cot[an]);
     int lgR = -1;
-    int64_t Bsel = 0;
+    int64_t Bmax = 0;
     for (int lg = 0; lg <= 3; ++lg) {
       if (forced > 0 && (1 << lg) != forced) continue;
       const int C = 32 >> lg;
       const double room = (C - 2) * hmin - rho;
       if (room < 0) continue;
-      const int64_t Bmax = (int64_t)std::floor(room / D) + 1;
       // fewest lanes per cell whose band fits: every lane then sweeps all members of its
       // cell (per-cell setup amortised over the most members)
-      if (Bmax >= 1) {
-        lgR = lg;
-        Bsel = std::min<int64_t>(Bmax, s->sc_pcap);
-        break;
-      }
+      lgR = lg;
+      Bmax = (int64_t)std::floor(room / D) + 1;
+      break;
     }
-    if (lgR < 0 || Bsel < 1)
+    if (lgR < 0 || Bmax < 1)
       throw Error(MOC_E_CAPACITY, "stack-collective sweep: a 2D segment rises through more layers than a warp has cells");
+    auto bands = [&](int g) {
+      const int64_t B = std::min<int64_t>(Bmax, s->sc_grp[g].pcap);
+      return (cnt + B - 1) / B;
+    };
+    int gsel = 0;
+    if (fctas) gsel = fctas - 3;
+    else
+      for (int g2 = 2; g2 > 0; --g2)
+        if (bands(g2) == bands(0)) {
+          gsel = g2;
+          break;
+        }
+    const int64_t Bsel = std::min<int64_t>(Bmax, s->sc_grp[gsel].pcap);
     for (int64_t b0 = 0; b0 < cnt; b0 += Bsel)
-      units.push_back(ScUnit{(uint32_t)q, (uint32_t)b0, (uint32_t)std::min<int64_t>(Bsel, cnt - b0), (uint32_t)lgR});
+      ug[gsel].push_back(ScUnit{(uint32_t)q, (uint32_t)b0, (uint32_t)std::min<int64_t>(Bsel, cnt - b0), (uint32_t)lgR});
+  }
+  std::vector<ScUnit> units;
+  for (int g2 = 0; g2 < 3; ++g2) {
+    s->sc_grp[g2].first = (uint32_t)units.size();
+    s->sc_grp[g2].n = (uint32_t)ug[g2].size();
+    units.insert(units.end(), ug[g2].begin(), ug[g2].end());
   }
   s->n_sc_units = (uint32_t)units.size();
   s->d_sc_units = dmalloc<ScUnit>(units.size(), Bytes);
@@ -1018,12 +1072,17 @@ void sc_configure(moc_solver* s, const Geometry& g, const Laydown& L, const std:
   k_sc_unit_cost<<<1024, 256, 0, st>>>(s->d_sc_units, s->n_sc_units, s->d_st_first, s->d_cost, keys);
   CUDA_OK(cudaGetLastError());
   auto pol = thrust::cuda::par.on(st);
-  thrust::stable_sort_by_key(pol, thrust::device_ptr<uint32_t>(keys), thrust::device_ptr<uint32_t>(keys) + units.size(),
-                             thrust::device_ptr<ScUnit>(s->d_sc_units), thrust::greater<uint32_t>());
+  for (int g2 = 0; g2 < 3; ++g2) {
+    const auto& q = s->sc_grp[g2];
+    if (q.n > 1)
+      thrust::stable_sort_by_key(pol, thrust::device_ptr<uint32_t>(keys) + q.first,
+                                 thrust::device_ptr<uint32_t>(keys) + q.first + q.n,
+                                 thrust::device_ptr<ScUnit>(s->d_sc_units) + q.first, thrust::greater<uint32_t>());
+  }
   CUDA_OK(cudaStreamSynchronize(st));
   cudaFree(keys);
   Bytes -= 4 * (int64_t)units.size();
-  s->d_counter = dmalloc<uint32_t>(2, Bytes);
+  s->d_counter = dmalloc<uint32_t>(4, Bytes);  // unit queues: one per occupancy group
   s->d_err = dmalloc<int>(1, Bytes);
   CUDA_OK(cudaMemsetAsync(s->d_err, 0, sizeof(int), st));
   s->d_tally32 = dmalloc<float>((size_t)s->J * s->GP + 8, Bytes);  // + tail for the leakage
@@ -1707,8 +1766,14 @@ int moc_get_timings(moc_solver* s, moc_timings* t) {
   t->iter_ms_last = s->iter_ms_last;
   // kernels per iteration: source, sweep, finalize, keff, normalize, resid (+ the two
   // bound kernels for schedule 0, + halo gather/scatter and leak park/restore for world > 1)
+  int sc_launches = 0;
+  for (int g = 0; g < 3; ++g) {
+    t->sc_units[g] = s->sc_grp[g].n;
+    sc_launches += s->sc_grp[g].n > 0;
+  }
   t->launches_per_iter = 6 + (s->opts.schedule == 0 ? 2 : 0) + (s->comm.world > 1 ? 4 : 0) +
-                         (s->exp_units > 0 && (int64_t)s->n_units > s->exp_units ? 1 : 0);  // EXP + OTF sweeps
+                         (s->exp_units > 0 && (int64_t)s->n_units > s->exp_units ? 1 : 0) +  // EXP + OTF sweeps
+                         (sc_launches > 1 ? sc_launches - 1 : 0);  // schedule 3: one sweep per occupancy group
   t->setup_ms = s->setup_ms;
   t->device_bytes = s->dev_bytes;
   t->exp_segments = s->exp_segments;

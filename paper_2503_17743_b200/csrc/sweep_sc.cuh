@@ -54,10 +54,10 @@ namespace {
 #endif
 constexpr int kScWarps = MOC_SC_WARPS;       // independent warps (units) per CTA
 constexpr int kScThreads = 32 * kScWarps;
-#ifndef MOC_SC_CTAS_PER_SM
-#define MOC_SC_CTAS_PER_SM 3
-#endif
-constexpr int kScMinBlocks = MOC_SC_CTAS_PER_SM;
+// CTAs per SM: the kernel is instantiated for 3, 4 and 5 (register caps 168 / 128 / 102;
+// the shared-memory psi band capacity shrinks as CTAs are added) and each stack is swept
+// by the instance with the most CTAs that does not cut it into more bands (solver.cu)
+constexpr int kScMinBlocksList[3] = {3, 4, 5};
 constexpr float kScSliverGuard = 4e-5f;      // fp32 corner length below which fp64 decides
 
 // debug statistics build (-DMOC_SC_STATS): per-sweep counts of the work decomposition
@@ -199,6 +199,31 @@ struct ScCell {
     return n;
   }
 
+#ifdef MOC_SC_PAIR
+  // visit() two members per trip with a predicated second member (one inlined copy of a
+  // two-member body, no separate tail copy): f2(m0, m1, has1), m1 == m0 when !has1
+  template <int STAT_TRIP, int STAT_CALL, class F2>
+  __device__ __forceinline__ int visit_pair(int a, int b, int r, int lgR, int c, F2&& f2) {
+    const int R = 1 << lgR;
+    const int a1 = a + ((r - a) & (R - 1));
+    if (a1 >= b) return 0;
+    const int n = ((b - 1 - a1) >> lgR) + 1;
+    int idx = ((((c << lgR) + r - a1) & 7) >> lgR);
+    if (idx >= n) idx = 0;
+#pragma unroll 1
+    for (int left = n; left > 0; left -= 2) {
+      const bool has1 = left > 1;
+      int i1 = idx + 1;
+      i1 = i1 == n ? 0 : i1;
+      i1 = has1 ? i1 : idx;
+      f2(a1 + (idx << lgR), a1 + (i1 << lgR), has1);
+      idx = i1 + 1;
+      idx = idx == n ? 0 : idx;
+    }
+    return n;
+  }
+#endif
+
   // shared-E class (Eq. 8 / Eq. 11 pieces of one cell, all of length L):
   // psi' = psi E + q (1 - E); T += (sum psi - n q)(1 - E)
   __device__ __forceinline__ void full(int a, int b, int r, int lgR, int c, float L) {
@@ -211,6 +236,26 @@ struct ScCell {
       qc[g] = q[g] * F[g];
       S[g] = 0.f;
     }
+#ifdef MOC_SC_PAIR
+    const int n = visit_pair<6, 8>(
+        a, b, r, lgR, c,
+        [&](int m0, int m1, bool has1) {
+          float v0[4 * NH], v1[4 * NH];
+          load(m0, v0);
+          load(m1, v1);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            S[g] += v0[g];
+            S[g] += has1 ? v1[g] : 0.f;
+            v0[g] = fmaf(v0[g], E[g], qc[g]);
+            v1[g] = fmaf(v1[g], E[g], qc[g]);
+          }
+          store(m1, v1);  // m1 == m0 without a second member: the same value, stored twice
+          store(m0, v0);
+          emit_hash(m0);
+          if (has1) emit_hash(m1);
+        });
+#else
     const int n = visit<6, 8>(
         a, b, r, lgR, c,
         [&](int m) {
@@ -224,6 +269,7 @@ struct ScCell {
           store(m, v);
           emit_hash(m);
         });
+#endif
     const float fn = (float)n;
 #pragma unroll
     for (int g = 0; g < G; ++g) T[g] = fmaf(fmaf(-fn, q[g], S[g]), F[g], T[g]);
@@ -320,8 +366,8 @@ struct ScCell {
   }
 };
 
-template <int G, int GP, bool HASH>
-__global__ void __launch_bounds__(kScThreads, kScMinBlocks) k_sweep_sc(ScArgs a) {
+template <int G, int GP, bool HASH, int MINB>
+__global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
   extern __shared__ __align__(16) float4 dsm_sc[];
   __shared__ double shP[2][kMaxPlanes + 1];  // canonical planes: [0] as given, [1] mirrored z' = Z - z
   __shared__ __align__(16) float4 shS4[kMaxMat * 2];  // sigma_t log2(e) per material, 8 groups

@@ -85,10 +85,12 @@ def test_cfg1_multigroup_k_inf(M, oracle_mod):
                                           (0, dict(v2_lane_stride=1)), (0, dict(v2_lane_stride=4)),
                                           (0, dict(v2_lane_stride=8)),
                                           (3, dict(sc_lanes_per_cell=2)), (3, dict(sc_lanes_per_cell=4)),
-                                          (3, dict(sc_lanes_per_cell=8))])
+                                          (3, dict(sc_lanes_per_cell=8)), (3, dict(sc_ctas_per_sm=3)),
+                                          (3, dict(sc_ctas_per_sm=4)), (3, dict(sc_ctas_per_sm=5))])
 def test_fixed_iteration_parity_small_lattice(M, oracle_mod, parity_log, schedule, opt):
-    """Every schedule, forced v2 lane strides 1/4/8 (the benched config runs at 4-8) and
-    forced stack-collective lanes per cell 2/4/8."""
+    """Every schedule, forced v2 lane strides 1/4/8 (the benched config runs at 4-8),
+    forced stack-collective lanes per cell 2/4/8 and each stack-collective occupancy
+    instance (3/4/5 CTAs per SM)."""
     prob = P.small_lattice(3, 3, 4)
     s = M.Solver(M.Problem(prob), schedule=schedule, **opt)
     k, _ = s.iterate(8)
@@ -268,3 +270,25 @@ def test_interleaved_solvers_keep_their_constants(M):
     assert ka == pytest.approx(alone[0][0], abs=1e-6) and kb == pytest.approx(alone[1][0], abs=1e-6)
     for s, (_, ref) in ((sa, alone[0]), (sb, alone[1])):
         assert np.abs(s.scalar_flux() - ref).max() / np.abs(ref).max() < 1e-5
+
+
+def test_sc_occupancy_groups(M):
+    """Stacks go to the occupancy instance with the most CTAs per SM that does not add
+    bands: small stacks (bands limited by the 30-layer window, not by shared memory) all run
+    at 5 CTAs per SM; a forced value puts every unit in its group; out of range is rejected."""
+    pr = M.Problem(P.small_lattice(3, 3, 4))
+    t = M.Solver(pr).timings()
+    n = sum(t["sc_units"])
+    assert t["sc_units"] == [0, 0, n] and n > 0
+    for c in (3, 4, 5):
+        t = M.Solver(pr, sc_ctas_per_sm=c).timings()
+        assert t["sc_units"][c - 3] == n and sum(t["sc_units"]) == n
+    with pytest.raises(M.MocError):
+        M.Solver(pr, sc_ctas_per_sm=6)
+    # a capacity cap below every group's own capacity: all groups band alike, so 5 CTAs
+    t = M.Solver(pr, sc_psi_cap=64).timings()
+    assert t["sc_units"][2] == sum(t["sc_units"])
+    # tall stacks at fine axial spacing (bands limited by shared memory): those stay at 3
+    prob = P.with_quadrature(P.small_lattice(2, 2, 40), axial_spacing=0.05)
+    t = M.Solver(M.Problem(prob)).timings()
+    assert t["sc_units"][0] > 0
