@@ -945,15 +945,16 @@ template <int G, int GP, int MINB>
 void sc_smem_configure_one(moc_solver* s, int g, int nsm) {
   cudaFuncAttributes fa{};
   CUDA_OK(cudaFuncGetAttributes(&fa, k_sweep_sc<G, GP, false, MINB>));
+  const size_t planes = sc_stage_smem(MINB) ? 0 : 2 * sizeof(double) * (size_t)sc_plane_stride(s->NL);
   const size_t per_cta = (228 * 1024) / MINB - 1024 - fa.sharedSizeBytes;
   constexpr int NH = ScH<G>::NH;
-  const size_t stage = (size_t)kScWarps * 32 * 64;  // per-warp cell staging (fast path)
-  int pcap = (int)((per_cta - stage) / ((size_t)kScWarps * NH * 16));
+  const size_t stage = sc_stage_smem(MINB) ? kScStageBytes : 0;
+  int pcap = (int)((per_cta - planes - stage) / ((size_t)kScWarps * NH * 16));
   if (s->opts.sc_psi_cap > 0) pcap = std::min(pcap, s->opts.sc_psi_cap);
   pcap = std::max(32, pcap & ~31);
   auto& q = s->sc_grp[g];
   q.pcap = pcap;
-  q.smem = (size_t)kScWarps * NH * pcap * 16 + stage;
+  q.smem = planes + (size_t)kScWarps * NH * pcap * 16 + stage;
   CUDA_OK(cudaFuncSetAttribute(k_sweep_sc<G, GP, false, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q.smem));
   int per_sm = 0;
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep_sc<G, GP, false, MINB>, kScThreads, q.smem));

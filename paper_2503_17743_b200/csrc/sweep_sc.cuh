@@ -68,6 +68,18 @@ __device__ unsigned long long g_sc_stats[16];
 #define SC_STAT(i, v) ((void)0)
 #endif
 
+// doubles per canonical plane copy in dynamic shared memory (NL + 1 planes, even count so
+// the psi bands that follow stay 16-byte aligned)
+__host__ __device__ constexpr int sc_plane_stride(int NL) { return (NL + 2) & ~1; }
+
+// 5 CTAs per SM (stacks whose bands are not limited by shared memory): static plane copies
+// and a shared staging area through which cell l + 1's source and sigma_t reach the corner
+// pieces of cell l (8 KB per CTA; fewer registers and instructions, the 102-register cap
+// spills otherwise).  3 and 4 CTAs per SM: the planes sized for NL in dynamic shared memory
+// and shuffles instead of the staging, every KB to the psi bands
+__host__ __device__ constexpr bool sc_stage_smem(int minb) { return minb >= 5; }
+constexpr size_t kScStageBytes = (size_t)kScWarps * 32 * 64;
+
 struct ScUnit {
   uint32_t stack, i0, n, lgR;  // members i0 .. i0+n-1 of the stack; R = 1 << lgR lanes per cell
 };
@@ -308,20 +320,15 @@ struct ScCell {
   // before the next plane.  Piece 1 (cell l): d1(m) = P_u - z_m = d1a + (b - 1 - m) dz;
   // piece 2 (cell l + 1, only if l + 1 is inside the domain): d2(m) = z_m + rho - P_u =
   // d2a + (m - a) dz; 3D length = d * ti.  A sliver piece (the walk merges it, App. A.7)
-  // gets length 0 (E = 1: no change) and is not emitted.  q2/sg2 = cell l + 1's source and
-  // sigma_t log2(e) (from the warp's cell staging); T2 = its tally share.
+  // gets length 0 (E = 1: no change) and is not emitted.  fetch2 gives cell l + 1's source
+  // and sigma_t log2(e) (q2, sg2); T2 = its tally share.
+  template <class Fetch2>
   __device__ __forceinline__ void corner2(int a, int b, int r, int lgR, int c, float d1a, float d2a, float dzf,
-                                          float ti, bool nxt, int skip1, int skip2, const float4* st2,
+                                          float ti, bool nxt, int skip1, int skip2, Fetch2&& fetch2,
                                           uint32_t j2, float* T2) {
     if (a >= b) return;
     float q2[8], sg2[8];
-    {
-      const float4 x0 = st2[0], x1 = st2[32], y0 = st2[64], y1 = st2[96];  // [4][32 lanes] float4
-      q2[0] = x0.x; q2[1] = x0.y; q2[2] = x0.z; q2[3] = x0.w;
-      q2[4] = x1.x; q2[5] = x1.y; q2[6] = x1.z; q2[7] = x1.w;
-      sg2[0] = y0.x; sg2[1] = y0.y; sg2[2] = y0.z; sg2[3] = y0.w;
-      sg2[4] = y1.x; sg2[5] = y1.y; sg2[6] = y1.z; sg2[7] = y1.w;
-    }
+    fetch2(q2, sg2);
     const float t2 = nxt ? ti : 0.f;  // no second piece above the domain top
     auto one = [&](int m, float* v) {
       const float L1 = m == skip1 ? 0.f : fmaf((float)(b - 1 - m), dzf, d1a) * ti;
@@ -368,15 +375,29 @@ struct ScCell {
 
 template <int G, int GP, bool HASH, int MINB>
 __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
+  // shared memory: the canonical planes (as given, and mirrored z' = Z - z), the warps' psi
+  // bands, then the cell staging (sc_stage_smem) or, HASH, the per-member hash state
   extern __shared__ __align__(16) float4 dsm_sc[];
-  __shared__ double shP[2][kMaxPlanes + 1];  // canonical planes: [0] as given, [1] mirrored z' = Z - z
   __shared__ __align__(16) float4 shS4[kMaxMat * 2];  // sigma_t log2(e) per material, 8 groups
   constexpr int NH = ScH<G>::NH;
   const DevData& d = a.d;
   const int NL = d.NL;
+  double* shP0;
+  double* shP1;
+  float4* band4;
+  if constexpr (sc_stage_smem(MINB)) {  // static plane copies (fixed addresses, fewer registers)
+    __shared__ double shPs[2][kMaxPlanes + 1];
+    shP0 = shPs[0];
+    shP1 = shPs[1];
+    band4 = dsm_sc;
+  } else {  // plane copies at the head of the dynamic shared memory, sized for NL
+    shP0 = reinterpret_cast<double*>(dsm_sc);
+    shP1 = shP0 + sc_plane_stride(NL);
+    band4 = dsm_sc + sc_plane_stride(NL);  // 2 x stride doubles = stride float4
+  }
   for (int q = threadIdx.x; q <= NL; q += blockDim.x) {
-    shP[0][q] = d.planes[q];
-    shP[1][q] = d.Z - d.planes[NL - q];
+    shP0[q] = d.planes[q];
+    shP1[q] = d.Z - d.planes[NL - q];
   }
   for (int q = threadIdx.x; q < kMaxMat * 8; q += blockDim.x) {
     const int m = q >> 3, g = q & 7;
@@ -385,10 +406,11 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pcap = a.pcap;
-  float4* const psl = dsm_sc + (size_t)warp * NH * pcap;
-  // per-warp cell staging (fast path), SoA [4][32 lanes] float4: q[0..7], sigma_t log2(e)[0..7]
-  float4* const stg = dsm_sc + (size_t)kScWarps * NH * pcap + (size_t)warp * 32 * 4;
-  float4* const hbase = dsm_sc + (size_t)kScWarps * NH * pcap + (size_t)kScWarps * 32 * 4;
+  float4* const psl = band4 + (size_t)warp * NH * pcap;
+  // per-warp cell staging, SoA [4][32 lanes] float4 (q[0..7], sigma_t log2(e)[0..7]), after
+  // the bands, only where shared memory is not the band limit (sc_stage_smem)
+  float4* const stg = band4 + (size_t)kScWarps * NH * pcap + (size_t)warp * 32 * 4;
+  float4* const hbase = band4 + (size_t)kScWarps * NH * pcap;
   uint64_t* const hh = HASH ? reinterpret_cast<uint64_t*>(hbase) + (size_t)warp * pcap : nullptr;
   int* const hc =
       HASH ? reinterpret_cast<int*>(reinterpret_cast<uint64_t*>(hbase) + (size_t)kScWarps * pcap) + (size_t)warp * pcap
@@ -426,7 +448,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
     for (int dir = 0; dir < 2; ++dir) {
       const bool ms = dir == 1;
       const bool mz = up == (dir == 1);
-      const double* P = shP[mz ? 1 : 0];
+      const double* P = mz ? shP1 : shP0;
       // canonical member m <-> physical member i0 + (mz ? B-1-m : m)
       for (int m = lane; m < B; m += 32) {
         const uint32_t id = id0 + (uint32_t)(mz ? B - 1 - m : m);
@@ -573,18 +595,44 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
         }
         const bool fast = rho < a.h_fast;  // every member crosses at most one plane here
         if (fast) {
-          if (!act) {  // finite staging for lanes without a cell (read only with zero lengths)
+          if (!act) {  // finite values for lanes without a cell, shuffled to corner pieces (read only with zero lengths)
 #pragma unroll
             for (int g = 0; g < 8; ++g) cell.q[g] = cell.sg[g] = 0.f;
           }
-          stg[lane] = make_float4(cell.q[0], cell.q[1], cell.q[2], cell.q[3]);
-          stg[32 + lane] = make_float4(cell.q[4], cell.q[5], cell.q[6], cell.q[7]);
-          stg[64 + lane] = make_float4(cell.sg[0], cell.sg[1], cell.sg[2], cell.sg[3]);
-          stg[96 + lane] = make_float4(cell.sg[4], cell.sg[5], cell.sg[6], cell.sg[7]);
-          __syncwarp();
+          // cell l + 1's source and sigma_t for the corner pieces entering it: through the
+          // warp's staging area, or by shuffles from its lanes (lane + R) after the full class
+          float q2s[8], sg2s[8];
+          if constexpr (sc_stage_smem(MINB)) {
+            stg[lane] = make_float4(cell.q[0], cell.q[1], cell.q[2], cell.q[3]);
+            stg[32 + lane] = make_float4(cell.q[4], cell.q[5], cell.q[6], cell.q[7]);
+            stg[64 + lane] = make_float4(cell.sg[0], cell.sg[1], cell.sg[2], cell.sg[3]);
+            stg[96 + lane] = make_float4(cell.sg[4], cell.sg[5], cell.sg[6], cell.sg[7]);
+            __syncwarp();
+          } else {
+            // members entering through the left face in layer l: full (Eq. 8)
+            if (act) cell.full(uPl, min(uPu, uPuR), r, lgR, ci, Lf);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              q2s[g] = g < G ? __shfl_sync(0xffffffffu, cell.q[g], (lane + R) & 31) : 0.f;
+              sg2s[g] = g < G ? __shfl_sync(0xffffffffu, cell.sg[g], (lane + R) & 31) : 0.f;
+            }
+          }
+          auto fetch2 = [&](float* q2, float* sg2) {
+            if constexpr (sc_stage_smem(MINB)) {
+              const float4* st2 = stg + ((lane + R) & 31);
+              const float4 x0 = st2[0], x1 = st2[32], y0 = st2[64], y1 = st2[96];
+              q2[0] = x0.x; q2[1] = x0.y; q2[2] = x0.z; q2[3] = x0.w;
+              q2[4] = x1.x; q2[5] = x1.y; q2[6] = x1.z; q2[7] = x1.w;
+              sg2[0] = y0.x; sg2[1] = y0.y; sg2[2] = y0.z; sg2[3] = y0.w;
+              sg2[4] = y1.x; sg2[5] = y1.y; sg2[6] = y1.z; sg2[7] = y1.w;
+            } else {
+#pragma unroll
+              for (int g = 0; g < 8; ++g) q2[g] = q2s[g], sg2[g] = sg2s[g];
+            }
+          };
           if (act) {
             // members entering through the left face in layer l: full (Eq. 8) ...
-            cell.full(uPl, min(uPu, uPuR), r, lgR, ci, Lf);
+            if constexpr (sc_stage_smem(MINB)) cell.full(uPl, min(uPu, uPuR), r, lgR, ci, Lf);
             // ... and corners, left -> top in l, bottom -> right in l + 1
             const int a0 = max(uPl, uPuR), b0 = uPu;
             if (a0 < b0) {
@@ -596,14 +644,14 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
               if ((float)d1 * ti < kScSliverGuard) {
                 const int mphys = mz ? B - 1 - (b0 - 1) : b0 - 1;
                 const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
-                if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) skip1 = b0 - 1;
+                if (sc_walk_len(d, shP0, sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) skip1 = b0 - 1;
               }
               if (nxt && (float)d2 * ti < kScSliverGuard) {
                 const int mphys = mz ? B - 1 - a0 : a0;
                 const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
-                if (sc_walk_len(d, shP[0], sb, k, lp2, z0, tn, isn, Lt, up) < kEpsL) skip2 = a0;
+                if (sc_walk_len(d, shP0, sb, k, lp2, z0, tn, isn, Lt, up) < kEpsL) skip2 = a0;
               }
-              cell.corner2(a0, b0, r, lgR, ci, (float)d1, (float)d2, dzf, ti, nxt, skip1, skip2, stg + ((lane + R) & 31),
+              cell.corner2(a0, b0, r, lgR, ci, (float)d1, (float)d2, dzf, ti, nxt, skip1, skip2, fetch2,
                            region * (uint32_t)NL + (uint32_t)lp2, T2);
             }
             // members entering through the domain bottom (canonical z' = 0) in this column
@@ -613,7 +661,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
               if ((float)dbot * ti < kScSliverGuard) {
                 const int mphys = mz ? B - 1 - a1 : a1;
                 const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
-                if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) ++a1;
+                if (sc_walk_len(d, shP0, sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) ++a1;
               }
               if (a1 < uPl)
                 cell.corner(a1, uPl, r, lgR, ci, a1, (float)(base + (double)a1 * dz + rho - Pl), dzf, ti);
@@ -637,7 +685,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
               if ((float)dtop * ti < kScSliverGuard) {
                 const int mphys = mz ? B - 1 - (b0 - 1) : b0 - 1;
                 const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
-                if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) --b0;
+                if (sc_walk_len(d, shP0, sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) --b0;
               }
               cell.corner(a0, b0, r, lgR, ci, b0 - 1, (float)(Pu - (base + (double)(b0 - 1) * dz)), dzf, ti);
             }
@@ -663,7 +711,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
                 if ((float)dbot * ti < kScSliverGuard) {
                   const int mphys = mz ? B - 1 - a1 : a1;
                   const double z0 = z0b + (double)(U.i0 + (uint32_t)mphys) * dz;
-                  if (sc_walk_len(d, shP[0], sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) ++a1;
+                  if (sc_walk_len(d, shP0, sb, k, lp, z0, tn, isn, Lt, up) < kEpsL) ++a1;
                 }
                 if (a1 < b1)
                   cell.corner(a1, b1, r, lgR, ci, a1, (float)(base + (double)a1 * dz + rho - Pl), dzf, ti);
