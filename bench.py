@@ -362,18 +362,23 @@ def run_ours(args):
     binding = None
     np_ = os.path.join(ROOT, "profiles", f"ncu_sweep_cfg{args.config}_s{args.schedule}.json")
     if os.path.exists(np_):
-        try:
-            mt = json.load(open(np_))[0]["metrics"]
-            binding = {"lsu_data_pipe_busy": float(mt["l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"][0]) / 100,
-                       "issue_active": float(mt["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]) / 100,
-                       "source": os.path.relpath(np_, ROOT)}
+        try:  # one sweep = one launch per occupancy group: duration-weighted over its launches
+            ks = [k["metrics"] for k in json.load(open(np_)) if "k_sweep" in k["kernel"]]
+            w = [float(m["gpu__time_duration.sum"][0]) for m in ks]
+
+            def avg(key):
+                return sum(wi * float(m[key][0]) for wi, m in zip(w, ks)) / sum(w) / 100
+
+            binding = {"lsu_data_pipe_busy": avg("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+                       "issue_active": avg("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                       "launches_per_sweep": len(ks), "source": os.path.relpath(np_, ROOT)}
         except Exception:
             binding = None
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_cfg{args.config}_s{args.schedule}.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            traffic = json.load(open(tp)).get("dram_bytes_per_sweep")
         except Exception:
             traffic = None
     line = {
@@ -393,7 +398,8 @@ def run_ours(args):
                    "backend": backend if world > 1 else None, "per_rank_ms": rank_ms,
                    "cuda_graph": True},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": UNIT, "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "k_sweep", "peak_basis":
+                     "traffic": traffic, "kernel": "k_sweep_sc (one sweep = one launch per occupancy group, timed together)",
+                     "peak_basis":
                          f"R_ALU = 148 SM x {mhz_max:.0f} MHz ({kind} sm_max) x 128 / (5 + 5/G), SURVEY 8(d)",
                      "frac_at_measured_clock": (achieved / r_alu(G, clocks["sm_mhz"]))
                      if clocks.get("sm_mhz") else None,
