@@ -699,6 +699,8 @@ void run_sweep_sc(moc_solver* s, unsigned long long* hash = nullptr, int32_t* ns
   a.nseg = nseg;
   a.gs = s->opts.gauss_seidel;
   a.slot_first = s->d_slot_first ? s->d_slot_first : s->d_st_first;
+  a.n_slots = (uint64_t)s->psi_slots;
+  a.n_fsr = (uint64_t)s->J;
   if constexpr (HASH) {  // every unit, 3 CTAs per SM (the largest band capacity)
     a.units = s->d_sc_units;
     a.n_units = s->n_sc_units;

@@ -80,6 +80,18 @@ __host__ __device__ constexpr int sc_plane_stride(int NL) { return (NL + 2) & ~1
 __host__ __device__ constexpr bool sc_stage_smem(int minb) { return minb >= 5; }
 constexpr size_t kScStageBytes = (size_t)kScWarps * 32 * 64;
 
+// bounds-checked debug build (-DMOC_SC_CHECK, tests run against it with MOC3D_LIB): every
+// shared-memory psi / hash index, plane index, FSR index and link target of the sweep is
+// checked and an out-of-range one traps (the kernel fails, the run reports a CUDA error)
+#ifdef MOC_SC_CHECK
+#define SC_CHECK(c) \
+  do {              \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define SC_CHECK(c) ((void)0)
+#endif
+
 struct ScUnit {
   uint32_t stack, i0, n, lgR;  // members i0 .. i0+n-1 of the stack; R = 1 << lgR lanes per cell
 };
@@ -105,6 +117,8 @@ struct ScArgs {
   int32_t* nseg;             // HASH: per slot emitted segment count
   int gs;                    // Gauss-Seidel (NEXT-4): psi_in == psi_out, slot pad word = write epoch
   const uint32_t* slot_first;  // per stack: first boundary-psi / link slot pair of its members on this rank
+  uint64_t n_slots;            // boundary-psi slots per buffer (bounds checks)
+  uint64_t n_fsr;              // FSRs (bounds checks)
 };
 
 template <int G>
@@ -154,6 +168,7 @@ struct ScCell {
   static constexpr int NH = ScH<G>::NH;
   float4* psl;  // psi halves [NH][pcap]
   int pcap;
+  int nb;       // members in the band (bounds checks)
   float q[8], sg[8], T[8];
   uint32_t j;
   uint64_t* hh;  // HASH state per member
@@ -161,6 +176,7 @@ struct ScCell {
   uint32_t nem;
 
   __device__ __forceinline__ void load(int m, float* v) const {
+    SC_CHECK(m >= 0 && m < nb && nb <= pcap);
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
       const float4 x = psl[h * pcap + m];
@@ -171,11 +187,13 @@ struct ScCell {
     }
   }
   __device__ __forceinline__ void store(int m, const float* v) {
+    SC_CHECK(m >= 0 && m < nb && nb <= pcap);
 #pragma unroll
     for (int h = 0; h < NH; ++h) psl[h * pcap + m] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
   }
   __device__ __forceinline__ void emit_hash(int m) {
     if constexpr (HASH) {
+      SC_CHECK(m >= 0 && m < nb);
       hh[m] = sc_fnv(hh[m], j);
       hc[m] += 1;
     }
@@ -485,6 +503,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
       ScCell<G, GP, HASH> cell;
       cell.psl = psl;
       cell.pcap = pcap;
+      cell.nb = B;
       cell.hh = hh;
       cell.hc = hc;
       cell.nem = 0;
@@ -570,6 +589,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
         if (act) {
           lp = mz ? NL - 1 - l : l;
           cell.j = region * (uint32_t)NL + (uint32_t)lp;
+          SC_CHECK(l >= 0 && l < NL && lp >= 0 && lp < NL && (uint64_t)cell.j < a.n_fsr);
           float qv[8];
           int mi;
           if constexpr (GP == 8) {
@@ -638,6 +658,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
             if (a0 < b0) {
               const bool nxt = l + 1 < NL;
               const int lp2 = mz ? lp - 1 : lp + 1;
+              SC_CHECK(!nxt || (lp2 >= 0 && lp2 < NL && l + 1 <= Lh));
               const double d1 = Pu - (base + (double)(b0 - 1) * dz);  // shortest piece 1: member b0 - 1
               const double d2 = base + (double)a0 * dz + rho - Pu;    // shortest piece 2: member a0
               int skip1 = -1, skip2 = -1;
@@ -700,6 +721,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
             const int e = l - q;  // entry layer (-1: through the domain bottom)
             if (act && e >= -1) {
               const int hi = uprev;  // Uf(P[e + 1])
+              SC_CHECK(e <= NL);
               const int ue = e >= 0 ? Uf(P[e]) : 0;
               uprev = ue;
               const int lo = max(ue, uPlR);
@@ -764,7 +786,9 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
         if constexpr (GP == 8 && G < 8) {
           if (a.gs) v[7] = __uint_as_float(ep);  // written in this sweep: current units
         }
+        SC_CHECK(2 * (uint64_t)id + dir < a.n_slots);
         const uint32_t out = a.link[2 * id + dir];
+        SC_CHECK(out == 0xffffffffu || out < a.n_slots);
         if (out != 0xffffffffu) {
           float* dst = a.psi_out + (size_t)out * GP;
           if constexpr (GP == 8) {
