@@ -212,6 +212,10 @@ struct ScCell {
     if (a1 >= b) return 0;
     const int n = ((b - 1 - a1) >> lgR) + 1;
     int idx = ((((c << lgR) + r - a1) & 7) >> lgR);
+    // a range shorter than the rotation: fold the start back into it (idx mod n for n >= 4),
+    // so lanes whose bank group is not in their range spread over it instead of all starting
+    // on its first member (consecutive cells' ranges start on nearly the same bank group)
+    if (idx >= n) idx -= n;
     if (idx >= n) idx = 0;
 #pragma unroll 1
     for (int left = n; left > 0; --left) {
@@ -229,30 +233,6 @@ struct ScCell {
     return n;
   }
 
-#ifdef MOC_SC_PAIR
-  // visit() two members per trip with a predicated second member (one inlined copy of a
-  // two-member body, no separate tail copy): f2(m0, m1, has1), m1 == m0 when !has1
-  template <int STAT_TRIP, int STAT_CALL, class F2>
-  __device__ __forceinline__ int visit_pair(int a, int b, int r, int lgR, int c, F2&& f2) {
-    const int R = 1 << lgR;
-    const int a1 = a + ((r - a) & (R - 1));
-    if (a1 >= b) return 0;
-    const int n = ((b - 1 - a1) >> lgR) + 1;
-    int idx = ((((c << lgR) + r - a1) & 7) >> lgR);
-    if (idx >= n) idx = 0;
-#pragma unroll 1
-    for (int left = n; left > 0; left -= 2) {
-      const bool has1 = left > 1;
-      int i1 = idx + 1;
-      i1 = i1 == n ? 0 : i1;
-      i1 = has1 ? i1 : idx;
-      f2(a1 + (idx << lgR), a1 + (i1 << lgR), has1);
-      idx = i1 + 1;
-      idx = idx == n ? 0 : idx;
-    }
-    return n;
-  }
-#endif
 
   // shared-E class (Eq. 8 / Eq. 11 pieces of one cell, all of length L):
   // psi' = psi E + q (1 - E); T += (sum psi - n q)(1 - E)
@@ -266,26 +246,6 @@ struct ScCell {
       qc[g] = q[g] * F[g];
       S[g] = 0.f;
     }
-#ifdef MOC_SC_PAIR
-    const int n = visit_pair<6, 8>(
-        a, b, r, lgR, c,
-        [&](int m0, int m1, bool has1) {
-          float v0[4 * NH], v1[4 * NH];
-          load(m0, v0);
-          load(m1, v1);
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            S[g] += v0[g];
-            S[g] += has1 ? v1[g] : 0.f;
-            v0[g] = fmaf(v0[g], E[g], qc[g]);
-            v1[g] = fmaf(v1[g], E[g], qc[g]);
-          }
-          store(m1, v1);  // m1 == m0 without a second member: the same value, stored twice
-          store(m0, v0);
-          emit_hash(m0);
-          if (has1) emit_hash(m1);
-        });
-#else
     const int n = visit<6, 8>(
         a, b, r, lgR, c,
         [&](int m) {
@@ -299,7 +259,6 @@ struct ScCell {
           store(m, v);
           emit_hash(m);
         });
-#endif
     const float fn = (float)n;
 #pragma unroll
     for (int g = 0; g < G; ++g) T[g] = fmaf(fmaf(-fn, q[g], S[g]), F[g], T[g]);
@@ -507,19 +466,13 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
       cell.hh = hh;
       cell.hc = hc;
       cell.nem = 0;
-#ifndef MOC_SC_NO_COLPF
-#define MOC_SC_COLPF 1
-#endif
-#ifdef MOC_SC_COLPF
       // column data prefetched 32 columns at a time (lane i holds column kk0 + i: its 2D
       // segment's two ends and region, one coalesced load each) and broadcast by shuffles
       double pf_sa = 0.0, pf_sb = 0.0;
       uint32_t pf_rg = 0;
-#endif
 #pragma unroll 1
       for (int kk = 0; kk < nk; ++kk) {
         const int k = ms ? nk - 1 - kk : kk;
-#ifdef MOC_SC_COLPF
         if ((kk & 31) == 0) {
           const int kq = kk + lane;
           if (kq < nk) {
@@ -531,11 +484,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
         }
         const double s_a = __shfl_sync(0xffffffffu, pf_sa, kk & 31);
         const double s_b = __shfl_sync(0xffffffffu, pf_sb, kk & 31);
-        const uint32_t region_pf = __shfl_sync(0xffffffffu, pf_rg, kk & 31);
-#else
-        const double s_a = k ? d.seg_send[sb + k - 1] : 0.0;
-        const double s_b = d.seg_send[sb + k];
-#endif
+        const uint32_t region = __shfl_sync(0xffffffffu, pf_rg, kk & 31);
         const double S = kk == 0 ? 0.0 : (ms ? Lt - s_b : s_a);
         const double w = s_b - s_a;
         const double base = zc0 + S * c, rho = w * c;
@@ -573,11 +522,6 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
           const int v = __double2int_ru((x - base) * invD);
           return min(max(v, 0), B);
         };
-#ifdef MOC_SC_COLPF
-        const uint32_t region = region_pf;
-#else
-        const uint32_t region = d.seg_region[sb + k];
-#endif
         const float Lf = (float)(w * isn);
 #pragma unroll
         for (int g = 0; g < 8; ++g) cell.T[g] = 0.f;
