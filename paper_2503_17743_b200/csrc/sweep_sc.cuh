@@ -217,12 +217,16 @@ struct ScCell {
     // on its first member (consecutive cells' ranges start on nearly the same bank group)
     if (idx >= n) idx -= n;
     if (idx >= n) idx = 0;
+    // iterate the member index itself (no per-trip index -> member shift), wrapping from
+    // the range end to a1, until back at the start
+    const int m0 = a1 + (idx << lgR), me = a1 + (n << lgR);
+    int m = m0;
 #pragma unroll 1
-    for (int left = n; left > 0; --left) {
-      f1(a1 + (idx << lgR));
-      ++idx;
-      idx = idx == n ? 0 : idx;
-    }
+    do {
+      f1(m);
+      m += R;
+      m = m == me ? a1 : m;
+    } while (m != m0);
 #ifdef MOC_SC_STATS
     {
       const unsigned am = __activemask();
