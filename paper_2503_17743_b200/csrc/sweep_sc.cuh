@@ -250,6 +250,49 @@ struct ScCell {
       qc[g] = q[g] * F[g];
       S[g] = 0.f;
     }
+#ifdef MOC_SC_FULL2
+    // packed FP32 over group pairs (FFMA2 / FADD2, each lane rounded as FFMA / FADD)
+    static_assert(NH == 2 || G <= 4, "FULL2 layout");
+    constexpr int NPF = G / 2;  // full pairs; an odd G's last group is scalar
+    float2 E2[4], Q2[4], S2[4];
+#pragma unroll
+    for (int p = 0; p < NPF; ++p) {
+      E2[p] = make_float2(E[2 * p], E[2 * p + 1]);
+      Q2[p] = make_float2(qc[2 * p], qc[2 * p + 1]);
+      S2[p] = make_float2(0.f, 0.f);
+    }
+    float Sl = 0.f;
+    const int n = visit<6, 8>(
+        a, b, r, lgR, c,
+        [&](int m) {
+          SC_CHECK(m >= 0 && m < nb && nb <= pcap);
+          float2* const p2 = reinterpret_cast<float2*>(psl);
+          float2 x[4];
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            const float4 t = psl[h * pcap + m];
+            x[2 * h] = make_float2(t.x, t.y);
+            x[2 * h + 1] = make_float2(t.z, t.w);
+          }
+#pragma unroll
+          for (int p = 0; p < NPF; ++p) {
+            S2[p] = __fadd2_rn(S2[p], x[p]);
+            x[p] = __ffma2_rn(x[p], E2[p], Q2[p]);
+          }
+          if constexpr (G & 1) {
+            float& xl = (G - 1) & 1 ? x[(G - 1) / 2].y : x[(G - 1) / 2].x;
+            Sl += xl;
+            xl = fmaf(xl, E[G - 1], qc[G - 1]);
+          }
+#pragma unroll
+          for (int p = 0; p < 2 * NH; ++p)
+            if (2 * p < G) p2[2 * ((p >> 1) * pcap + m) + (p & 1)] = x[p];
+          emit_hash(m);
+        });
+#pragma unroll
+    for (int p = 0; p < NPF; ++p) S[2 * p] = S2[p].x, S[2 * p + 1] = S2[p].y;
+    if constexpr (G & 1) S[G - 1] = Sl;
+#else
     const int n = visit<6, 8>(
         a, b, r, lgR, c,
         [&](int m) {
@@ -263,6 +306,7 @@ struct ScCell {
           store(m, v);
           emit_hash(m);
         });
+#endif
     const float fn = (float)n;
 #pragma unroll
     for (int g = 0; g < G; ++g) T[g] = fmaf(fmaf(-fn, q[g], S[g]), F[g], T[g]);
