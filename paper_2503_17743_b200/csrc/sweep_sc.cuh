@@ -250,9 +250,10 @@ struct ScCell {
       qc[g] = q[g] * F[g];
       S[g] = 0.f;
     }
-#ifdef MOC_SC_FULL2
-    // packed FP32 over group pairs (FFMA2 / FADD2, each lane rounded as FFMA / FADD)
-    static_assert(NH == 2 || G <= 4, "FULL2 layout");
+    // packed FP32 over group pairs (FFMA2 / FADD2, each lane rounded as FFMA / FADD: the
+    // same results as the one-group form), an odd G's last group scalar: 20 instructions
+    // per member instead of 27
+    static_assert(NH == 2 || G <= 4, "psi halves layout");
     constexpr int NPF = G / 2;  // full pairs; an odd G's last group is scalar
     float2 E2[4], Q2[4], S2[4];
 #pragma unroll
@@ -292,21 +293,6 @@ struct ScCell {
 #pragma unroll
     for (int p = 0; p < NPF; ++p) S[2 * p] = S2[p].x, S[2 * p + 1] = S2[p].y;
     if constexpr (G & 1) S[G - 1] = Sl;
-#else
-    const int n = visit<6, 8>(
-        a, b, r, lgR, c,
-        [&](int m) {
-          float v[4 * NH];
-          load(m, v);
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            S[g] += v[g];
-            v[g] = fmaf(v[g], E[g], qc[g]);
-          }
-          store(m, v);
-          emit_hash(m);
-        });
-#endif
     const float fn = (float)n;
 #pragma unroll
     for (int g = 0; g < G; ++g) T[g] = fmaf(fmaf(-fn, q[g], S[g]), F[g], T[g]);
