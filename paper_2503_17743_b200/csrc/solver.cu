@@ -950,7 +950,7 @@ void sc_smem_configure_one(moc_solver* s, int g, int nsm) {
   const size_t planes = sc_stage_smem(MINB) ? 0 : 2 * sizeof(double) * (size_t)sc_plane_stride(s->NL);
   const size_t per_cta = (228 * 1024) / MINB - 1024 - fa.sharedSizeBytes;
   constexpr int NH = ScH<G>::NH;
-  const size_t stage = sc_stage_smem(MINB) ? kScStageBytes : 0;
+  const size_t stage = sc_stage_smem(MINB) ? sc_stage_bytes<G>() : 0;
   int pcap = (int)((per_cta - planes - stage) / ((size_t)kScWarps * NH * 16));
   if (s->opts.sc_psi_cap > 0) pcap = std::min(pcap, s->opts.sc_psi_cap);
   pcap = std::max(32, pcap & ~31);

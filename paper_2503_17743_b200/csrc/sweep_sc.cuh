@@ -73,12 +73,15 @@ __device__ unsigned long long g_sc_stats[16];
 __host__ __device__ constexpr int sc_plane_stride(int NL) { return (NL + 2) & ~1; }
 
 // 5 CTAs per SM (stacks whose bands are not limited by shared memory): static plane copies
-// and a shared staging area through which cell l + 1's source and sigma_t reach the corner
-// pieces of cell l (8 KB per CTA; fewer registers and instructions, the 102-register cap
-// spills otherwise).  3 and 4 CTAs per SM: the planes sized for NL in dynamic shared memory
+// and a shared staging area through which cell l + 1's source and material (sigma_t from
+// the per-CTA table) reach the corner pieces of cell l (4 KB per CTA for G < 8; fewer
+// registers and instructions, the 102-register cap spills otherwise).  3 and 4 CTAs per SM: the planes sized for NL in dynamic shared memory
 // and shuffles instead of the staging, every KB to the psi bands
 __host__ __device__ constexpr bool sc_stage_smem(int minb) { return minb >= 5; }
-constexpr size_t kScStageBytes = (size_t)kScWarps * 32 * 64;
+// staging per warp: [2][32 lanes] float4 (q[0..6] + the material index) for G < 8, else
+// [4][32 lanes] (q[0..7], sigma_t log2(e)[0..7])
+template <int G>
+constexpr size_t sc_stage_bytes() { return (size_t)kScWarps * 32 * (G < 8 ? 32 : 64); }
 
 // bounds-checked debug build (-DMOC_SC_CHECK, tests run against it with MOC3D_LIB): every
 // shared-memory psi / hash index, plane index, FSR index and link target of the sweep is
@@ -418,9 +421,9 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int pcap = a.pcap;
   float4* const psl = band4 + (size_t)warp * NH * pcap;
-  // per-warp cell staging, SoA [4][32 lanes] float4 (q[0..7], sigma_t log2(e)[0..7]), after
-  // the bands, only where shared memory is not the band limit (sc_stage_smem)
-  float4* const stg = band4 + (size_t)kScWarps * NH * pcap + (size_t)warp * 32 * 4;
+  // per-warp cell staging (sc_stage_bytes) after the bands, only where shared memory is not
+  // the band limit (sc_stage_smem)
+  float4* const stg = band4 + (size_t)kScWarps * NH * pcap + (size_t)warp * 32 * (G < 8 ? 2 : 4);
   float4* const hbase = band4 + (size_t)kScWarps * NH * pcap;
   uint64_t* const hh = HASH ? reinterpret_cast<uint64_t*>(hbase) + (size_t)warp * pcap : nullptr;
   int* const hc =
@@ -564,12 +567,12 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
         for (int g = 0; g < 8; ++g) T2[g] = 0.f;
         double Pl = 0, Pu = 0;
         int uPl = 0, uPu = 0, uPlR = 0, uPuR = 0, lp = 0;
+        int mi = 0;  // the cell's material
         if (act) {
           lp = mz ? NL - 1 - l : l;
           cell.j = region * (uint32_t)NL + (uint32_t)lp;
           SC_CHECK(l >= 0 && l < NL && lp >= 0 && lp < NL && (uint64_t)cell.j < a.n_fsr);
           float qv[8];
-          int mi;
           if constexpr (GP == 8) {
             const float4 x0 = tex1Dfetch<float4>(a.qtex, (int)(2 * cell.j)), x1 = tex1Dfetch<float4>(a.qtex, (int)(2 * cell.j + 1));
             qv[0] = x0.x; qv[1] = x0.y; qv[2] = x0.z; qv[3] = x0.w;
@@ -602,9 +605,13 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
           float q2s[8], sg2s[8];
           if constexpr (sc_stage_smem(MINB)) {
             stg[lane] = make_float4(cell.q[0], cell.q[1], cell.q[2], cell.q[3]);
-            stg[32 + lane] = make_float4(cell.q[4], cell.q[5], cell.q[6], cell.q[7]);
-            stg[64 + lane] = make_float4(cell.sg[0], cell.sg[1], cell.sg[2], cell.sg[3]);
-            stg[96 + lane] = make_float4(cell.sg[4], cell.sg[5], cell.sg[6], cell.sg[7]);
+            if constexpr (G < 8) {  // the material index in the free eighth word: Sigma_t from shS4
+              stg[32 + lane] = make_float4(cell.q[4], cell.q[5], cell.q[6], __int_as_float(act ? mi : 0));
+            } else {
+              stg[32 + lane] = make_float4(cell.q[4], cell.q[5], cell.q[6], cell.q[7]);
+              stg[64 + lane] = make_float4(cell.sg[0], cell.sg[1], cell.sg[2], cell.sg[3]);
+              stg[96 + lane] = make_float4(cell.sg[4], cell.sg[5], cell.sg[6], cell.sg[7]);
+            }
             __syncwarp();
           } else {
             // members entering through the left face in layer l: full (Eq. 8)
@@ -618,9 +625,18 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
           auto fetch2 = [&](float* q2, float* sg2) {
             if constexpr (sc_stage_smem(MINB)) {
               const float4* st2 = stg + ((lane + R) & 31);
-              const float4 x0 = st2[0], x1 = st2[32], y0 = st2[64], y1 = st2[96];
+              const float4 x0 = st2[0], x1 = st2[32];
+              float4 y0, y1;
+              if constexpr (G < 8) {
+                const int mi2 = __float_as_int(x1.w);
+                y0 = shS4[2 * mi2];
+                y1 = shS4[2 * mi2 + 1];
+              } else {
+                y0 = st2[64];
+                y1 = st2[96];
+              }
               q2[0] = x0.x; q2[1] = x0.y; q2[2] = x0.z; q2[3] = x0.w;
-              q2[4] = x1.x; q2[5] = x1.y; q2[6] = x1.z; q2[7] = x1.w;
+              q2[4] = x1.x; q2[5] = x1.y; q2[6] = x1.z; q2[7] = G < 8 ? 0.f : x1.w;
               sg2[0] = y0.x; sg2[1] = y0.y; sg2[2] = y0.z; sg2[3] = y0.w;
               sg2[4] = y1.x; sg2[5] = y1.y; sg2[6] = y1.z; sg2[7] = y1.w;
             } else {
