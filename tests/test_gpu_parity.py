@@ -101,17 +101,20 @@ def test_fixed_iteration_parity_small_lattice(M, oracle_mod, parity_log, schedul
     np.testing.assert_allclose(kh, ref["k_hist"], atol=TOL_K)
 
 
-@pytest.mark.parametrize("schedule", [0, 3])
-@pytest.mark.parametrize("G", [1, 2, 3, 4, 5, 8])
-def test_other_group_counts_parity(M, oracle_mod, parity_log, G, schedule):
-    """Every group-count instantiation of the sweep (G = 1, 2, 3 -> 4, 4, 5 -> 8 padded,
-    and G = 8 where the source has no pad slot and the material comes from mat[])."""
+@pytest.mark.parametrize("schedule,ctas", [(0, 0), (3, 0), (3, 3)])
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 5, 6, 8])
+def test_other_group_counts_parity(M, oracle_mod, parity_log, G, schedule, ctas):
+    """Every group-count instantiation of the sweep (G = 1, 2, 3 -> 4, 4, 5, 6 -> 8 padded,
+    and G = 8 where the source has no pad slot and the material comes from mat[]); for the
+    stack-collective sweep both the 5-CTA instance the small stacks get (static planes, cell
+    staging) and the forced 3-CTA one (dynamic planes, shuffled cell data)."""
     prob = P.small_lattice(3, 3, 4, xs=P.xs_synthetic(G))
-    s = M.Solver(M.Problem(prob), schedule=schedule)
+    s = M.Solver(M.Problem(prob), schedule=schedule, **({"sc_ctas_per_sm": ctas} if ctas else {}))
     k, _ = s.iterate(6)
     _check_emitted(s)
     ref = oracle_mod.Oracle(prob).solve(fixed_iters=6)
-    _check(parity_log, f"small_lattice_G{G}_it6_s{schedule}", k, ref["k"], s.scalar_flux(), ref["phi"])
+    _check(parity_log, f"small_lattice_G{G}_it6_s{schedule}" + (f"_ctas{ctas}" if ctas else ""), k, ref["k"],
+           s.scalar_flux(), ref["phi"])
 
 
 @pytest.mark.parametrize("tile_cells", [4, 9, 37])
