@@ -303,6 +303,96 @@ struct ScCell {
     SC_STAT(3, n);
   }
 
+  // members full in this cell in two consecutive columns (same layer, same lanes): both
+  // updates in one visit, Eq. 3 with this column's (E, q (1 - E)) then the next column's
+  // (E', q' (1 - E')); this column's tally as full(), the next column's partial sum Sn and
+  // count nn carried to it (addff).  Hash: this cell's id j, then the next cell's j2.
+  __device__ __forceinline__ void fullff(int a, int b, int r, int lgR, int c, float L, const float* q2,
+                                         const float* sg2, float L2, uint32_t j2, float* Sn, int& nn) {
+    nn = 0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) Sn[g] = 0.f;
+    if (a >= b) return;
+    constexpr int NPF = G / 2;
+    float E[8], F[8], qc[8], Eb[8], qcb[8];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      E[g] = ex2_approx(-sg[g] * L);
+      F[g] = 1.f - E[g];
+      qc[g] = q[g] * F[g];
+      Eb[g] = ex2_approx(-sg2[g] * L2);
+      qcb[g] = q2[g] * (1.f - Eb[g]);
+    }
+    float2 E2[4], Q2[4], S2[4], Eb2[4], Qb2[4], Sb2[4];
+#pragma unroll
+    for (int p = 0; p < NPF; ++p) {
+      E2[p] = make_float2(E[2 * p], E[2 * p + 1]);
+      Q2[p] = make_float2(qc[2 * p], qc[2 * p + 1]);
+      Eb2[p] = make_float2(Eb[2 * p], Eb[2 * p + 1]);
+      Qb2[p] = make_float2(qcb[2 * p], qcb[2 * p + 1]);
+      S2[p] = Sb2[p] = make_float2(0.f, 0.f);
+    }
+    float Sl = 0.f, Sbl = 0.f;
+    const int n = visit<6, 8>(
+        a, b, r, lgR, c,
+        [&](int m) {
+          SC_CHECK(m >= 0 && m < nb && nb <= pcap);
+          float2* const p2 = reinterpret_cast<float2*>(psl);
+          float2 x[4];
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            const float4 t = psl[h * pcap + m];
+            x[2 * h] = make_float2(t.x, t.y);
+            x[2 * h + 1] = make_float2(t.z, t.w);
+          }
+#pragma unroll
+          for (int p = 0; p < NPF; ++p) {
+            S2[p] = __fadd2_rn(S2[p], x[p]);
+            x[p] = __ffma2_rn(x[p], E2[p], Q2[p]);
+            Sb2[p] = __fadd2_rn(Sb2[p], x[p]);
+            x[p] = __ffma2_rn(x[p], Eb2[p], Qb2[p]);
+          }
+          if constexpr (G & 1) {
+            float& xl = (G - 1) & 1 ? x[(G - 1) / 2].y : x[(G - 1) / 2].x;
+            Sl += xl;
+            xl = fmaf(xl, E[G - 1], qc[G - 1]);
+            Sbl += xl;
+            xl = fmaf(xl, Eb[G - 1], qcb[G - 1]);
+          }
+#pragma unroll
+          for (int p = 0; p < 2 * NH; ++p)
+            if (2 * p < G) p2[2 * ((p >> 1) * pcap + m) + (p & 1)] = x[p];
+          if constexpr (HASH) {
+            emit_hash(m);
+            hh[m] = sc_fnv(hh[m], j2);
+            hc[m] += 1;
+          }
+        });
+    float S[8];
+#pragma unroll
+    for (int p = 0; p < NPF; ++p) {
+      S[2 * p] = S2[p].x, S[2 * p + 1] = S2[p].y;
+      Sn[2 * p] = Sb2[p].x, Sn[2 * p + 1] = Sb2[p].y;
+    }
+    if constexpr (G & 1) S[G - 1] = Sl, Sn[G - 1] = Sbl;
+    const float fn = (float)n;
+#pragma unroll
+    for (int g = 0; g < G; ++g) T[g] = fmaf(fmaf(-fn, q[g], S[g]), F[g], T[g]);
+    nn = n;
+    nem += 2 * n;
+    SC_STAT(3, 2 * n);
+  }
+  // the carried part of this cell's tally: (1 - E)(Sn - nn q) of the members fullff swept
+  __device__ __forceinline__ void addff(const float* Sn, int nn, float L) {
+    if (nn == 0) return;
+    const float fn = (float)nn;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float F = 1.f - ex2_approx(-sg[g] * L);
+      T[g] = fmaf(fmaf(-fn, q[g], Sn[g]), F, T[g]);
+    }
+  }
+
   // corner class: length d(m) * ti with d = d0 + |m - anchor| dz (anchor = shortest member);
   // per member Eq. 3: dpsi = (psi - q)(1 - E), psi -= dpsi, T += dpsi
   __device__ __forceinline__ void corner(int a, int b, int r, int lgR, int c, int anchor, float d0, float dzf,
@@ -507,6 +597,11 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
       // segment's two ends and region, one coalesced load each) and broadcast by shuffles
       double pf_sa = 0.0, pf_sb = 0.0;
       uint32_t pf_rg = 0;
+      // two-column visits (fullff): this column's fused members were swept in the previous
+      // one (fzr); their member range [fzA, fzB) and carried tally part (fzS, fzN)
+      bool fzr = false;
+      int fzA = 0, fzB = 0, fzN = 0;
+      float fzS[8];
 #pragma unroll 1
       for (int kk = 0; kk < nk; ++kk) {
         const int k = ms ? nk - 1 - kk : kk;
@@ -595,6 +690,29 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
           uPu = Uf(Pu);
         }
         const bool fast = rho < a.h_fast;  // every member crosses at most one plane here
+        // fuse with the next column when it is in this prefetch block, also takes the fast
+        // path and keeps the band window (so the same lane owns each layer in both): the
+        // same expressions the next column evaluates, so both agree bit for bit.  Only at 3
+        // CTAs per SM: there it cuts the shared-memory wavefronts by 22 % (ncu) and the time
+        // by 2.6 %; at 4 CTAs it measured slower, at 5 the registers would spill
+        bool fzs = false;
+        double base2 = 0.0, rho2 = 0.0;
+        float Lf2 = 0.f;
+        uint32_t region2 = 0;
+        if constexpr (MINB == 3) {
+          const int kn = (kk + 1) & 31;
+          const double sa2 = __shfl_sync(0xffffffffu, pf_sa, kn), sb2 = __shfl_sync(0xffffffffu, pf_sb, kn);
+          region2 = __shfl_sync(0xffffffffu, pf_rg, kn);
+          if (fast && !fzr && kk + 1 < nk && kn != 0) {
+            const double S2 = ms ? Lt - sb2 : sa2;
+            const double w2 = sb2 - sa2;
+            base2 = zc0 + S2 * c;
+            rho2 = w2 * c;
+            const double top2 = base2 + (double)(B - 1) * dz + rho2;
+            fzs = rho2 < a.h_fast && base2 < d.Z && top2 > 0.0 && PnLo > base2 && PnHi >= top2;
+            Lf2 = (float)(w2 * isn);
+          }
+        }
         if (fast) {
           if (!act) {  // finite values for lanes without a cell, shuffled to corner pieces (read only with zero lengths)
 #pragma unroll
@@ -615,7 +733,45 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
             __syncwarp();
           } else {
             // members entering through the left face in layer l: full (Eq. 8)
-            if (act) cell.full(uPl, min(uPu, uPuR), r, lgR, ci, Lf);
+            if (act) {
+              const int e1 = min(uPu, uPuR);
+              if (fzr) {  // the fused members [fzA, fzB) were swept with the previous column
+                cell.full(uPl, min(fzA, e1), r, lgR, ci, Lf);
+                cell.full(max(fzB, uPl), e1, r, lgR, ci, Lf);
+                cell.addff(fzS, fzN, Lf);
+              } else if (fzs) {
+                // the next column's cell in this layer: source, material, Sigma_t
+                const uint32_t j2 = region2 * (uint32_t)NL + (uint32_t)lp;
+                SC_CHECK((uint64_t)j2 < a.n_fsr);
+                float q2f[8], sg2f[8];
+                {
+                  float qv[8];
+                  int mi2;
+                  if constexpr (GP == 8) {
+                    const float4 x0 = tex1Dfetch<float4>(a.qtex, (int)(2 * j2)), x1 = tex1Dfetch<float4>(a.qtex, (int)(2 * j2 + 1));
+                    qv[0] = x0.x; qv[1] = x0.y; qv[2] = x0.z; qv[3] = x0.w;
+                    qv[4] = x1.x; qv[5] = x1.y; qv[6] = x1.z; qv[7] = x1.w;
+                  } else {
+                    load_q<GP>(a.qt, (int64_t)j2, qv);
+                  }
+                  if constexpr (G < GP) mi2 = __float_as_int(qv[G]);
+                  else mi2 = a.mat[j2];
+                  const float4 s0 = shS4[2 * mi2], s1 = shS4[2 * mi2 + 1];
+                  sg2f[0] = s0.x; sg2f[1] = s0.y; sg2f[2] = s0.z; sg2f[3] = s0.w;
+                  sg2f[4] = s1.x; sg2f[5] = s1.y; sg2f[6] = s1.z; sg2f[7] = s1.w;
+#pragma unroll
+                  for (int g = 0; g < 8; ++g) q2f[g] = g < G ? qv[g] : 0.f;
+                }
+                const int uPuR2 = min(max(__double2int_ru((Pu - rho2 - base2) * invD), 0), B);
+                const int ffb = max(min(e1, uPuR2), uPl);
+                cell.fullff(uPl, ffb, r, lgR, ci, Lf, q2f, sg2f, Lf2, j2, fzS, fzN);
+                cell.full(ffb, e1, r, lgR, ci, Lf);
+                fzA = uPl;
+                fzB = ffb;
+              } else {
+                cell.full(uPl, e1, r, lgR, ci, Lf);
+              }
+            }
 #pragma unroll
             for (int g = 0; g < 8; ++g) {
               q2s[g] = g < G ? __shfl_sync(0xffffffffu, cell.q[g], (lane + R) & 31) : 0.f;
@@ -760,6 +916,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
             }
           }
         }
+        fzr = fzs;
         __syncwarp();
       }
       nemit += cell.nem;
