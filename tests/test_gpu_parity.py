@@ -86,11 +86,14 @@ def test_cfg1_multigroup_k_inf(M, oracle_mod):
                                           (0, dict(v2_lane_stride=8)),
                                           (3, dict(sc_lanes_per_cell=2)), (3, dict(sc_lanes_per_cell=4)),
                                           (3, dict(sc_lanes_per_cell=8)), (3, dict(sc_ctas_per_sm=3)),
-                                          (3, dict(sc_ctas_per_sm=4)), (3, dict(sc_ctas_per_sm=5))])
+                                          (3, dict(sc_ctas_per_sm=4)), (3, dict(sc_ctas_per_sm=5)),
+                                          (3, dict(sc_ctas_per_sm=3, sc_lanes_per_cell=2)),
+                                          (3, dict(sc_ctas_per_sm=3, sc_lanes_per_cell=4))])
 def test_fixed_iteration_parity_small_lattice(M, oracle_mod, parity_log, schedule, opt):
     """Every schedule, forced v2 lane strides 1/4/8 (the benched config runs at 4-8),
-    forced stack-collective lanes per cell 2/4/8 and each stack-collective occupancy
-    instance (3/4/5 CTAs per SM)."""
+    forced stack-collective lanes per cell 2/4/8, each stack-collective occupancy instance
+    (3/4/5 CTAs per SM) and the 3-CTA instance's two-column visits with 2 and 4 lanes per
+    cell."""
     prob = P.small_lattice(3, 3, 4)
     s = M.Solver(M.Problem(prob), schedule=schedule, **opt)
     k, _ = s.iterate(8)
