@@ -721,6 +721,46 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
           // cell l + 1's source and sigma_t for the corner pieces entering it: through the
           // warp's staging area, or by shuffles from its lanes (lane + R) after the full class
           float q2s[8], sg2s[8];
+          // the full class (Eq. 8), with the two-column visits of a fused column pair
+          auto full_class = [&]() {
+            const int e1 = min(uPu, uPuR);
+            if (fzr) {  // the fused members [fzA, fzB) were swept with the previous column
+              cell.full(uPl, min(fzA, e1), r, lgR, ci, Lf);
+              cell.full(max(fzB, uPl), e1, r, lgR, ci, Lf);
+              cell.addff(fzS, fzN, Lf);
+            } else if (fzs) {
+              // the next column's cell in this layer: source, material, Sigma_t
+              const uint32_t j2 = region2 * (uint32_t)NL + (uint32_t)lp;
+              SC_CHECK((uint64_t)j2 < a.n_fsr);
+              float q2f[8], sg2f[8];
+              {
+                float qv[8];
+                int mi2;
+                if constexpr (GP == 8) {
+                  const float4 x0 = tex1Dfetch<float4>(a.qtex, (int)(2 * j2)), x1 = tex1Dfetch<float4>(a.qtex, (int)(2 * j2 + 1));
+                  qv[0] = x0.x; qv[1] = x0.y; qv[2] = x0.z; qv[3] = x0.w;
+                  qv[4] = x1.x; qv[5] = x1.y; qv[6] = x1.z; qv[7] = x1.w;
+                } else {
+                  load_q<GP>(a.qt, (int64_t)j2, qv);
+                }
+                if constexpr (G < GP) mi2 = __float_as_int(qv[G]);
+                else mi2 = a.mat[j2];
+                const float4 s0 = shS4[2 * mi2], s1 = shS4[2 * mi2 + 1];
+                sg2f[0] = s0.x; sg2f[1] = s0.y; sg2f[2] = s0.z; sg2f[3] = s0.w;
+                sg2f[4] = s1.x; sg2f[5] = s1.y; sg2f[6] = s1.z; sg2f[7] = s1.w;
+#pragma unroll
+                for (int g = 0; g < 8; ++g) q2f[g] = g < G ? qv[g] : 0.f;
+              }
+              const int uPuR2 = min(max(__double2int_ru((Pu - rho2 - base2) * invD), 0), B);
+              const int ffb = max(min(e1, uPuR2), uPl);
+              cell.fullff(uPl, ffb, r, lgR, ci, Lf, q2f, sg2f, Lf2, j2, fzS, fzN);
+              cell.full(ffb, e1, r, lgR, ci, Lf);
+              fzA = uPl;
+              fzB = ffb;
+            } else {
+              cell.full(uPl, e1, r, lgR, ci, Lf);
+            }
+          };
           if constexpr (sc_stage_smem(MINB)) {
             stg[lane] = make_float4(cell.q[0], cell.q[1], cell.q[2], cell.q[3]);
             if constexpr (G < 8) {  // the material index in the free eighth word: Sigma_t from shS4
@@ -733,45 +773,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
             __syncwarp();
           } else {
             // members entering through the left face in layer l: full (Eq. 8)
-            if (act) {
-              const int e1 = min(uPu, uPuR);
-              if (fzr) {  // the fused members [fzA, fzB) were swept with the previous column
-                cell.full(uPl, min(fzA, e1), r, lgR, ci, Lf);
-                cell.full(max(fzB, uPl), e1, r, lgR, ci, Lf);
-                cell.addff(fzS, fzN, Lf);
-              } else if (fzs) {
-                // the next column's cell in this layer: source, material, Sigma_t
-                const uint32_t j2 = region2 * (uint32_t)NL + (uint32_t)lp;
-                SC_CHECK((uint64_t)j2 < a.n_fsr);
-                float q2f[8], sg2f[8];
-                {
-                  float qv[8];
-                  int mi2;
-                  if constexpr (GP == 8) {
-                    const float4 x0 = tex1Dfetch<float4>(a.qtex, (int)(2 * j2)), x1 = tex1Dfetch<float4>(a.qtex, (int)(2 * j2 + 1));
-                    qv[0] = x0.x; qv[1] = x0.y; qv[2] = x0.z; qv[3] = x0.w;
-                    qv[4] = x1.x; qv[5] = x1.y; qv[6] = x1.z; qv[7] = x1.w;
-                  } else {
-                    load_q<GP>(a.qt, (int64_t)j2, qv);
-                  }
-                  if constexpr (G < GP) mi2 = __float_as_int(qv[G]);
-                  else mi2 = a.mat[j2];
-                  const float4 s0 = shS4[2 * mi2], s1 = shS4[2 * mi2 + 1];
-                  sg2f[0] = s0.x; sg2f[1] = s0.y; sg2f[2] = s0.z; sg2f[3] = s0.w;
-                  sg2f[4] = s1.x; sg2f[5] = s1.y; sg2f[6] = s1.z; sg2f[7] = s1.w;
-#pragma unroll
-                  for (int g = 0; g < 8; ++g) q2f[g] = g < G ? qv[g] : 0.f;
-                }
-                const int uPuR2 = min(max(__double2int_ru((Pu - rho2 - base2) * invD), 0), B);
-                const int ffb = max(min(e1, uPuR2), uPl);
-                cell.fullff(uPl, ffb, r, lgR, ci, Lf, q2f, sg2f, Lf2, j2, fzS, fzN);
-                cell.full(ffb, e1, r, lgR, ci, Lf);
-                fzA = uPl;
-                fzB = ffb;
-              } else {
-                cell.full(uPl, e1, r, lgR, ci, Lf);
-              }
-            }
+            if (act) full_class();
 #pragma unroll
             for (int g = 0; g < 8; ++g) {
               q2s[g] = g < G ? __shfl_sync(0xffffffffu, cell.q[g], (lane + R) & 31) : 0.f;
@@ -802,7 +804,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
           };
           if (act) {
             // members entering through the left face in layer l: full (Eq. 8) ...
-            if constexpr (sc_stage_smem(MINB)) cell.full(uPl, min(uPu, uPuR), r, lgR, ci, Lf);
+            if constexpr (sc_stage_smem(MINB)) full_class();
             // ... and corners, left -> top in l, bottom -> right in l + 1
             const int a0 = max(uPl, uPuR), b0 = uPu;
             if (a0 < b0) {
