@@ -1059,8 +1059,23 @@ void sc_configure(moc_solver* s, const Geometry& g, const Laydown& L, const std:
           break;
         }
     const int64_t Bsel = std::min<int64_t>(Bmax, s->sc_grp[gsel].pcap);
+    // 5 CTAs per SM: skewed shared-memory slots (sweep_sc.cuh ScCell::slot), one spare slot
+    // every ~1/alpha members, so the member ranges of consecutive cells (P = h / dz apart)
+    // start on different 16-byte bank groups even when P is close to a multiple of 8; alpha
+    // aims at an odd slot distance and is capped by the band capacity
+    uint32_t skew = 0;
+    if (gsel == 2 && Bsel > 1) {
+      const double Pm = hmin / D;
+      double T = std::ceil(Pm);
+      if (std::fmod(T, 2.0) == 0.0) T += 1.0;
+      const int64_t pc = s->sc_grp[2].pcap;
+      const double alpha = std::min(T / Pm - 1.0, (double)(pc - 1) / (double)(Bsel - 1) - 1.0);
+      if (alpha > 0) skew = (uint32_t)std::min(65535.0, std::floor(alpha * 65536.0));
+      while (skew && (Bsel - 1) + (int64_t)(((uint32_t)(Bsel - 1) * skew) >> 16) > pc - 1) --skew;
+    }
     for (int64_t b0 = 0; b0 < cnt; b0 += Bsel)
-      ug[gsel].push_back(ScUnit{(uint32_t)q, (uint32_t)b0, (uint32_t)std::min<int64_t>(Bsel, cnt - b0), (uint32_t)lgR});
+      ug[gsel].push_back(ScUnit{(uint32_t)q, (uint32_t)b0, (uint32_t)std::min<int64_t>(Bsel, cnt - b0),
+                                (uint32_t)lgR | (skew << 16)});
   }
   std::vector<ScUnit> units;
   for (int g2 = 0; g2 < 3; ++g2) {

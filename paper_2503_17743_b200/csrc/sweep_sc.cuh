@@ -96,7 +96,8 @@ constexpr size_t sc_stage_bytes() { return (size_t)kScWarps * 32 * (G < 8 ? 32 :
 #endif
 
 struct ScUnit {
-  uint32_t stack, i0, n, lgR;  // members i0 .. i0+n-1 of the stack; R = 1 << lgR lanes per cell
+  uint32_t stack, i0, n;  // members i0 .. i0+n-1 of the stack
+  uint32_t lgR;           // bits 0-7: R = 1 << lgR lanes per cell; bits 16-31: slot skew (5 CTAs)
 };
 
 struct ScArgs {
@@ -166,7 +167,7 @@ __device__ __forceinline__ uint64_t sc_fnv(uint64_t h, uint32_t u) {
   return h;
 }
 
-template <int G, int GP, bool HASH>
+template <int G, int GP, bool HASH, bool SK = false>
 struct ScCell {
   static constexpr int NH = ScH<G>::NH;
   float4* psl;  // psi halves [NH][pcap]
@@ -177,12 +178,17 @@ struct ScCell {
   uint64_t* hh;  // HASH state per member
   int* hc;
   uint32_t nem;
+  uint32_t skew = 0;  // SK: shared-memory slot of member m = m + (m skew) >> 16 (sc_configure)
+  __device__ __forceinline__ int slot(int m) const {
+    if constexpr (SK) return m + (int)(((uint32_t)m * skew) >> 16);
+    else return m;
+  }
 
   __device__ __forceinline__ void load(int m, float* v) const {
-    SC_CHECK(m >= 0 && m < nb && nb <= pcap);
+    SC_CHECK(m >= 0 && m < nb && slot(nb - 1) < pcap);
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
-      const float4 x = psl[h * pcap + m];
+      const float4 x = psl[h * pcap + slot(m)];
       v[4 * h] = x.x;
       v[4 * h + 1] = x.y;
       v[4 * h + 2] = x.z;
@@ -190,9 +196,9 @@ struct ScCell {
     }
   }
   __device__ __forceinline__ void store(int m, const float* v) {
-    SC_CHECK(m >= 0 && m < nb && nb <= pcap);
+    SC_CHECK(m >= 0 && m < nb && slot(nb - 1) < pcap);
 #pragma unroll
-    for (int h = 0; h < NH; ++h) psl[h * pcap + m] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+    for (int h = 0; h < NH; ++h) psl[h * pcap + slot(m)] = make_float4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
   }
   __device__ __forceinline__ void emit_hash(int m) {
     if constexpr (HASH) {
@@ -214,7 +220,7 @@ struct ScCell {
     const int a1 = a + ((r - a) & (R - 1));
     if (a1 >= b) return 0;
     const int n = ((b - 1 - a1) >> lgR) + 1;
-    int idx = ((((c << lgR) + r - a1) & 7) >> lgR);
+    int idx = ((((c << lgR) + r - slot(a1)) & 7) >> lgR);
     // a range shorter than the rotation: fold the start back into it (idx mod n for n >= 4),
     // so lanes whose bank group is not in their range spread over it instead of all starting
     // on its first member (consecutive cells' ranges start on nearly the same bank group)
@@ -269,12 +275,12 @@ struct ScCell {
     const int n = visit<6, 8>(
         a, b, r, lgR, c,
         [&](int m) {
-          SC_CHECK(m >= 0 && m < nb && nb <= pcap);
+          SC_CHECK(m >= 0 && m < nb && slot(nb - 1) < pcap);
           float2* const p2 = reinterpret_cast<float2*>(psl);
           float2 x[4];
 #pragma unroll
           for (int h = 0; h < NH; ++h) {
-            const float4 t = psl[h * pcap + m];
+            const float4 t = psl[h * pcap + slot(m)];
             x[2 * h] = make_float2(t.x, t.y);
             x[2 * h + 1] = make_float2(t.z, t.w);
           }
@@ -290,7 +296,7 @@ struct ScCell {
           }
 #pragma unroll
           for (int p = 0; p < 2 * NH; ++p)
-            if (2 * p < G) p2[2 * ((p >> 1) * pcap + m) + (p & 1)] = x[p];
+            if (2 * p < G) p2[2 * ((p >> 1) * pcap + slot(m)) + (p & 1)] = x[p];
           emit_hash(m);
         });
 #pragma unroll
@@ -336,12 +342,12 @@ struct ScCell {
     const int n = visit<6, 8>(
         a, b, r, lgR, c,
         [&](int m) {
-          SC_CHECK(m >= 0 && m < nb && nb <= pcap);
+          SC_CHECK(m >= 0 && m < nb && slot(nb - 1) < pcap);
           float2* const p2 = reinterpret_cast<float2*>(psl);
           float2 x[4];
 #pragma unroll
           for (int h = 0; h < NH; ++h) {
-            const float4 t = psl[h * pcap + m];
+            const float4 t = psl[h * pcap + slot(m)];
             x[2 * h] = make_float2(t.x, t.y);
             x[2 * h + 1] = make_float2(t.z, t.w);
           }
@@ -361,7 +367,7 @@ struct ScCell {
           }
 #pragma unroll
           for (int p = 0; p < 2 * NH; ++p)
-            if (2 * p < G) p2[2 * ((p >> 1) * pcap + m) + (p & 1)] = x[p];
+            if (2 * p < G) p2[2 * ((p >> 1) * pcap + slot(m)) + (p & 1)] = x[p];
           if constexpr (HASH) {
             emit_hash(m);
             hh[m] = sc_fnv(hh[m], j2);
@@ -540,7 +546,12 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
     const double c = fabs(cot), invD = 1.0 / dz;
     const float ti = (float)(isn * fabs(tn));  // 3D length per unit of z: 1/|cos(theta)|
     const float dzf = (float)dz;
-    const int B = (int)U.n, lgRu = (int)U.lgR;
+    const int B = (int)U.n, lgRu = (int)(U.lgR & 0xffu);
+    const uint32_t skw = U.lgR >> 16;  // the band's shared-memory slot skew (5 CTAs per SM)
+    auto slot_of = [&](int m) {
+      if constexpr (MINB == 5 && !HASH) return m + (int)(((uint32_t)m * skw) >> 16);
+      else return m;
+    };
     // largest R for a column: keep >= 3 members of a full cell per lane (hmin / dz members
     // per cell), below which the per-lane cell setup outweighs the split member work
     int lgRcap = lgRu;
@@ -567,7 +578,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
         }
 #pragma unroll
         for (int h = 0; h < NH; ++h)
-          psl[h * pcap + m] = make_float4(v[4 * h] * sc_, 4 * h + 1 < G ? v[4 * h + 1] * sc_ : 0.f,
+          psl[h * pcap + slot_of(m)] = make_float4(v[4 * h] * sc_, 4 * h + 1 < G ? v[4 * h + 1] * sc_ : 0.f,
                                           4 * h + 2 < G ? v[4 * h + 2] * sc_ : 0.f, 4 * h + 3 < G ? v[4 * h + 3] * sc_ : 0.f);
         if constexpr (HASH) {
           hh[m] = kFnvInit;
@@ -586,7 +597,8 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
       double PnLo = NL > 1 ? P[1] : kInf, PnHi = PnLo;
       if (lane == 0) SC_STAT(0, 1);
       __syncwarp();
-      ScCell<G, GP, HASH> cell;
+      ScCell<G, GP, HASH, MINB == 5 && !HASH> cell;
+      cell.skew = skw;
       cell.psl = psl;
       cell.pcap = pcap;
       cell.nb = B;
@@ -928,7 +940,7 @@ __global__ void __launch_bounds__(kScThreads, MINB) k_sweep_sc(ScArgs a) {
         float v[8];
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
-          const float4 x = psl[h * pcap + m];
+          const float4 x = psl[h * pcap + slot_of(m)];
           v[4 * h] = x.x;
           v[4 * h + 1] = x.y;
           v[4 * h + 2] = x.z;
